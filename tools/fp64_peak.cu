@@ -1,0 +1,42 @@
+// Microbenchmark: FP64 FMA peak and HBM streaming bandwidth on the box (for the
+// roofline denominators DESIGN.md derives; MEASURED_PEAKS.json has no FP64 number).
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void dfma_loop(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+__global__ void copy_k(const double2* __restrict__ a, double2* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) b[i] = a[i];
+}
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out; cudaMalloc(&out, sizeof(double) * sms * 8 * 1024);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int iters = 20000;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    dfma_loop<<<sms * 8, 256>>>(out, iters);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * 8 * iters * (double)sms * 8 * 256;
+    printf("fp64 fma: %.2f TFLOP/s (%.3f ms)\n", flops / ms / 1e9, ms);
+  }
+  size_t n = (size_t)1 << 27;  // 2 GiB per buffer of double2
+  double2 *a, *b; cudaMalloc(&a, n * 16); cudaMalloc(&b, n * 16);
+  cudaMemset(a, 0, n * 16);
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    copy_k<<<sms * 16, 512>>>(a, b, n);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("copy: %.1f GB/s\n", 2.0 * n * 16 / ms / 1e6);
+  }
+  return 0;
+}
