@@ -1,0 +1,156 @@
+/*
+ * lorpc.h — C ABI of the B200-native LOR additive-Schwarz preconditioned PCG
+ * hot path of arXiv 1908.07071 ("Matrix-free preconditioners for high-order
+ * continuous and discontinuous Galerkin discretizations").
+ *
+ * Citations: "P:n" = PAPER.md line n (section / \label named); readings "cN"
+ * are listed in DESIGN.md §Readings.
+ *
+ * Conventions (all entry points):
+ *  - Return value: LORPC_OK (0) or an lorpc_status error code.  No exceptions
+ *    or exit() cross the ABI; a human-readable diagnostic of the last error on
+ *    the calling thread is available from lorpc_last_error().
+ *  - Pointers ending in `_dev` are CUDA device pointers (FP64 unless stated),
+ *    owned by the caller, which must keep them alive until the stream work that
+ *    uses them has completed.  `_host` pointers are host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All apply calls are asynchronous on that stream; setup calls and
+ *    lorpc_pcg_solve synchronize the stream before returning.
+ *  - Handles (lorpc_mesh, lorpc_lor, lorpc_prec) own their device workspaces,
+ *    allocated at create/setup time and never inside apply/solve; destroy frees
+ *    them.  A lorpc_lor / lorpc_prec references its mesh, which must outlive it.
+ *  - Layout: CG vectors have one entry per GLL node of the global node grid
+ *    (n_0 p + 1) x (n_1 p + 1) [x (n_2 p + 1)], x fastest, Dirichlet (grid
+ *    boundary) entries present.  DG vectors are element-major
+ *    [n_el][(p+1)^d], elements x-fastest, local nodes x-fastest.
+ *  - Mesh: Cartesian topology n_0 x n_1 [x n_2] of tensor-product elements, each
+ *    the image of [0,1]^d under the multilinear map of its 2^d vertices
+ *    (P:82-84); vertices [(n_0+1)(n_1+1)[(n_2+1)]][d], x fastest.
+ */
+#ifndef LORPC_H
+#define LORPC_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LORPC_OK = 0,
+  LORPC_ERR_ARG = 1,              /* invalid argument (NULL, p < 1, eta <= 0, ...) */
+  LORPC_ERR_SIZE = 2,             /* unsupported size (p outside the compiled set, ...) */
+  LORPC_ERR_INVERTED_ELEMENT = 3, /* det J <= 0 at a quadrature point (element id in message) */
+  LORPC_ERR_ZERO_PIVOT = 4,       /* ILU(0) pivot <= 0 (patch, level, step in message) */
+  LORPC_ERR_BREAKDOWN = 5,        /* PCG p.Ap <= 0 or r.z <= 0 (iteration in message) */
+  LORPC_ERR_NOT_CONVERGED = 6,    /* PCG hit maxit */
+  LORPC_ERR_CUDA = 7,             /* CUDA runtime error */
+  LORPC_ERR_OOM = 8               /* device allocation failed */
+} lorpc_status;
+
+typedef struct lorpc_mesh lorpc_mesh;
+typedef struct lorpc_lor lorpc_lor;
+typedef struct lorpc_prec lorpc_prec;
+
+/* Discretisation (P:82-105 CG, eq:ip P:113-136 SIPG). */
+typedef struct {
+  int dim;      /* 2 or 3 */
+  int n[3];     /* elements per axis (n[2] ignored in 2D) */
+  int p;        /* polynomial degree; compiled set: 2D p in {2..8}, 3D p in {2..6} */
+  int disc;     /* 0 = continuous H1 (CG), 1 = symmetric interior penalty DG */
+  double eta;   /* SIPG only: sigma_e = eta / h_e, h_e = min(|K-|,|K+|)/|e| (readings c13, c14) */
+} lorpc_mesh_desc;
+
+/* Additive Schwarz B = sum_{j=0}^J R_j Q_j (eq:as P:274-277). */
+typedef struct {
+  int patch_kind; /* 0 = vertex patches (eq:patch P:302-315), 1 = element star (reading c9) */
+  int ordering;   /* ILU(0) ordering: 0 = minimum discarded fill, 1 = natural */
+  int coarse;     /* 0 = R_0 one GMG V(1,1) with l1-Jacobi (reading c11), 1 = no coarse term */
+} lorpc_schwarz_desc;
+
+typedef struct {
+  int iters;          /* operator applications performed */
+  int converged;      /* 1 if ||r||_2 <= rtol ||b||_2 */
+  double rel_res;     /* final ||r||_2 / ||b||_2 (recursively updated residual) */
+  double* res_hist;   /* host, caller-owned, length >= maxit+1, or NULL */
+  double* alpha;      /* host, length >= maxit, or NULL (Lanczos kappa) */
+  double* beta;       /* host, length >= maxit, or NULL */
+  double t_solve_ms;  /* device time of the iteration loop (CUDA events) */
+} lorpc_pcg_report;
+
+/* ---- mesh / geometry (a1) ------------------------------------------------- */
+/* Creates the mesh, uploads the vertices, computes geometric factors
+ * G_q = w_q det J_q J_q^{-1} J_q^{-T} at the q^d Gauss points (q = p+1,
+ * reading c1) and checks det J > 0 (LORPC_ERR_INVERTED_ELEMENT). */
+int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, void* stream,
+                      lorpc_mesh** out);
+void lorpc_mesh_destroy(lorpc_mesh* m);
+/* Sizes: n_dof = length of the solution vector (CG nodes or DG dofs), n_quad =
+ * number of volume quadrature points, n_bface_quad = boundary-face quadrature
+ * points (DG weak Dirichlet data, reading c15; 0 for CG). */
+int lorpc_mesh_sizes(const lorpc_mesh* m, long long* n_dof, long long* n_quad, long long* n_bface_quad);
+/* Physical coordinates [n_quad][d] of the volume Gauss points (element-major,
+ * x-fastest) and [n_bface_quad][d] of the boundary-face Gauss points (ordering:
+ * axis, side low/high, elements ascending, face points lower axis fastest);
+ * either output may be NULL. */
+int lorpc_quad_points(const lorpc_mesh* m, double* xq_dev, double* xbq_dev, void* stream);
+/* Load vector b = (f, v) (eq:fem) from f at the volume Gauss points; CG:
+ * Dirichlet rows zeroed; DG: plus the symmetric Nitsche boundary data
+ * int_e (sigma_e g v - g d_n v) from g at the boundary points (gq_dev may be
+ * NULL for g = 0). */
+int lorpc_rhs_assemble(const lorpc_mesh* m, const double* fq_dev, const double* gq_dev,
+                       double* b_dev, void* stream);
+
+/* ---- operator (a2, a3) ------------------------------------------------------ */
+/* y = A x, matrix-free by sum factorisation (tab:complexity P:764).
+ * CG: y_F = K_FF x_F, y_D = x_D (symmetric Dirichlet elimination).
+ * SIPG: volume term plus interior/boundary face terms of eq:ip.
+ * x_dev and y_dev must not alias. */
+int lorpc_operator_apply(const lorpc_mesh* m, const double* x_dev, double* y_dev, void* stream);
+
+/* ---- LOR (a11) ---------------------------------------------------------------- */
+/* Assembles K_h, the Q1 stiffness on the GLL-refined mesh (exact
+ * multilinear subcell maps with 2^d Gauss points, reading c2), and the
+ * element-structured Galerkin hierarchy A_{l+1} = P_l^T A_l P_l (P:549-555,
+ * readings c3, c4).  For a DG mesh the CG LOR of the same mesh and p is built
+ * (R_p of eq:dg-as). */
+int lorpc_lor_assemble(const lorpc_mesh* m, void* stream, lorpc_lor** out);
+void lorpc_lor_destroy(lorpc_lor* l);
+
+/* ---- Schwarz setup (a5-a9, a11) ------------------------------------------------ */
+/* Patches, per-patch per-level ordering (MDF, reading c6) fused with the ILU(0)
+ * elimination into M = L D L^T (reading c5), level schedules, the coarse-space
+ * GMG hierarchy (reading c11) and, for DG, D_B = diag(A_IP) on element-boundary
+ * DG nodes (reading c16).  Errors: LORPC_ERR_ZERO_PIVOT. */
+int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void* stream,
+                        lorpc_prec** out);
+void lorpc_prec_destroy(lorpc_prec* b);
+/* z = B r (eq:as); CG: z_D = 0.  DG: z = E B(E^T r) + S_B D_B^{-1} S_B^T r
+ * (eq:dg-as P:635-641).  r_dev and z_dev must not alias. */
+int lorpc_precond_apply(const lorpc_prec* b, const double* r_dev, double* z_dev, void* stream);
+/* Copies the elimination order (patch-local natural indices, step order) of
+ * patch `patch` at hierarchy level `level` to perm_host (capacity *n on input;
+ * the patch size on output). */
+int lorpc_prec_export_ordering(const lorpc_prec* b, long long patch, int level, int* perm_host, int* n);
+/* Number of patches and hierarchy levels. */
+int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels);
+
+/* ---- PCG (a10) ------------------------------------------------------------------ */
+/* Preconditioned conjugate gradients (reading c12): x_0 = 0,
+ * stop when ||r_k||_2 <= rtol ||b||_2.  x_dev is overwritten.  Device-resident
+ * vectors; synchronizes the stream.  Returns LORPC_ERR_NOT_CONVERGED or
+ * LORPC_ERR_BREAKDOWN with the report filled up to the last iteration. */
+int lorpc_pcg_solve(const lorpc_mesh* m, const lorpc_prec* b, const double* b_dev, double* x_dev,
+                    double rtol, int maxit, lorpc_pcg_report* rep, void* stream);
+/* Same solve with host buffers: copies b_host in and x_host out inside the
+ * call (the end-to-end path the bench's e2e number times). */
+int lorpc_pcg_solve_host(const lorpc_mesh* m, const lorpc_prec* b, const double* b_host, double* x_host,
+                         double rtol, int maxit, lorpc_pcg_report* rep, void* stream);
+
+/* Number of kernel launches issued by this library on the calling thread since
+ * the last reset (instrumentation for the bench's gpu_launches claim). */
+long long lorpc_launch_count(int reset);
+const char* lorpc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LORPC_H */

@@ -1,0 +1,151 @@
+// Internal header of the lorpc CUDA library (sm_100a, FP64).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/lorpc.h"
+
+namespace lorpc {
+
+constexpr int MAXP = 8;          // largest compiled polynomial degree
+constexpr int MAXL = 6;          // hierarchy levels (ceil(log2 p) + 1 <= 4 for p <= 8)
+constexpr int MAXC = 12;         // coarse GMG levels
+
+// ---- error handling -------------------------------------------------------------
+void set_error(const std::string& s);
+int fail(int code, const std::string& s);
+long long& launch_counter();
+#define LORPC_CUDA(call)                                                              \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return ::lorpc::fail(LORPC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define LORPC_LAUNCHED()                                                              \
+  do {                                                                                \
+    ++::lorpc::launch_counter();                                                      \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess)                                                            \
+      return ::lorpc::fail(LORPC_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+#define LORPC_TRY(call)                 \
+  do {                                  \
+    int rc_ = (call);                   \
+    if (rc_ != LORPC_OK) return rc_;    \
+  } while (0)
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) { *p = nullptr; return LORPC_OK; }
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) return fail(LORPC_ERR_OOM, "cudaMalloc " + std::to_string(n * sizeof(T)) + " B");
+  return LORPC_OK;
+}
+template <class T>
+void dfree(T*& p) { if (p) cudaFree((void*)p); p = nullptr; }
+
+// ---- 1D basis tables (kernel parameters; constant bank) ----------------------------
+struct Basis1D {
+  int p, q;
+  double xi[MAXP + 1];              // GLL nodes on [0,1]
+  double wq[MAXP + 1];              // Gauss weights on [0,1] (q = p+1, reading c1)
+  double xq[MAXP + 1];              // Gauss nodes
+  double B[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j(x_q)
+  double D[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j'(x_q)
+  double E0[MAXP + 1], E1[MAXP + 1];  // l_j'(0), l_j'(1) (face normal derivatives)
+};
+void make_basis(int p, Basis1D& b);                 // basis.cpp
+std::vector<std::vector<int>> make_chain(int p);    // basis.cpp (reading c3)
+
+// Per-element-local 1D prolongation table between hierarchy levels l+1 -> l:
+// fine local index t in [0, mf): coarse local indices c0[t], c1[t] and weights.
+struct Transfer1D {
+  int mf, mc, gap;
+  int c0[MAXP + 1], c1[MAXP + 1];   // coarse local indices of fine local t
+  double w0[MAXP + 1], w1[MAXP + 1];
+  int ret[MAXP + 1];                // fine local index of coarse local index
+};
+
+struct Grid { int d; int n[3]; };  // elements per axis
+
+}  // namespace lorpc
+
+// ---- opaque handles -----------------------------------------------------------------
+struct lorpc_mesh {
+  lorpc_mesh_desc desc;
+  int d, p, q, nloc, nq;            // nq = q^d
+  int n[3], N[3];                   // elements / GLL nodes per axis (1 in unused axis)
+  long long nel, ndof_cg, ndof, nquad, nbq;
+  lorpc::Basis1D basis;
+  double* V = nullptr;              // [nvert][d]
+  double* G = nullptr;              // [nel][ncomp][nq] geometric factors
+  double* X = nullptr;              // [ndof_cg][d] node coordinates
+  double* vol = nullptr;            // [nel] element volumes (DG)
+  double* dgdiag = nullptr;         // [ndof] diag(A_IP) (DG)
+  double* ywork = nullptr;          // DG face workspace
+};
+
+struct lorpc_lor {
+  const lorpc_mesh* m;
+  int L;                            // hierarchy levels (finest 0)
+  int ml[lorpc::MAXL];              // nodes per element per axis at level l
+  int Nax[lorpc::MAXL][3];          // level node grid per axis
+  long long Nl[lorpc::MAXL];
+  double* A[lorpc::MAXL];           // full 3^d stencil [ND][N_l], column = node
+  lorpc::Transfer1D T[lorpc::MAXL]; // T[l]: level l+1 -> l
+};
+
+struct lorpc_prec {
+  const lorpc_lor* lor;
+  const lorpc_mesh* m;
+  lorpc_schwarz_desc desc;
+  long long J;                      // patches
+  int L;
+  int max_n[lorpc::MAXL];           // largest patch size per level
+  char* rec = nullptr;              // per patch-level ILU records
+  long long* recoff = nullptr;      // [J][L] byte offsets
+  std::vector<long long> recoff_h;
+  long long rec_bytes = 0;
+  // coarse space (R_0)
+  int nc = 0;                       // GMG levels
+  int cn[lorpc::MAXC][3];           // vertices per axis
+  long long cN[lorpc::MAXC];
+  double* Ac[lorpc::MAXC];          // full stencil; Ac[0] aliases lor->A[L-1]
+  double* dl1[lorpc::MAXC];
+  double* cr[lorpc::MAXC];
+  double* cz[lorpc::MAXC];
+  double* cs[lorpc::MAXC];
+  double* coarse_chol = nullptr;    // dense LDL^T of the coarsest GMG level
+  int ncoarsest = 0;
+  // DG workspace
+  double* rcg = nullptr;
+  double* zcg = nullptr;
+  // PCG workspace
+  double *r = nullptr, *z = nullptr, *pv = nullptr, *qv = nullptr;
+  double* scal = nullptr;           // device scalars
+  double* part = nullptr;           // reduction partials
+  double* hostpin = nullptr;        // pinned scalars
+  double* xb = nullptr;             // host-buffer solve staging (b, x)
+  cudaStream_t aux = nullptr;       // second stream (coarse chain)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace lorpc {
+// internal entry points shared between translation units
+int geom_setup(lorpc_mesh* m, cudaStream_t s);
+int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s);
+int dg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s);
+int dg_diag_setup(lorpc_mesh* m, cudaStream_t s);
+int dg_restrict_cg(const lorpc_mesh* m, const double* r_dg, double* r_cg, cudaStream_t s);
+int dg_combine(const lorpc_mesh* m, const double* r_dg, const double* z_cg, double* z_dg, cudaStream_t s);
+int lor_build(const lorpc_mesh* m, lorpc_lor* l, cudaStream_t s);
+int schwarz_build(lorpc_prec* b, cudaStream_t s);
+int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
+int quad_points(const lorpc_mesh* m, double* xq, double* xbq, cudaStream_t s);
+int rhs_assemble(const lorpc_mesh* m, const double* fq, const double* gq, double* b, cudaStream_t s);
+int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double* x, double rtol,
+            int maxit, lorpc_pcg_report* rep, cudaStream_t s);
+}  // namespace lorpc

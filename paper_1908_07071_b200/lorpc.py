@@ -1,0 +1,211 @@
+"""Thin ctypes binding of the lorpc C ABI (include/lorpc.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+of liblorpc.so.  Device vectors are torch CUDA float64 tensors (torch supplies
+device memory and streams); host arrays are numpy float64.  There is no CPU
+fallback: if liblorpc.so is missing or a call fails, an exception is raised.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblorpc.so")
+_lib = None
+
+_vp = ctypes.c_void_p
+_int = ctypes.c_int
+_ll = ctypes.c_longlong
+_d = ctypes.c_double
+
+
+class LorpcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"lorpc error {code}: {msg}")
+        self.code = code
+
+
+class MeshDesc(ctypes.Structure):
+    _fields_ = [("dim", _int), ("n", _int * 3), ("p", _int), ("disc", _int), ("eta", _d)]
+
+
+class SchwarzDesc(ctypes.Structure):
+    _fields_ = [("patch_kind", _int), ("ordering", _int), ("coarse", _int)]
+
+
+class PcgReport(ctypes.Structure):
+    _fields_ = [("iters", _int), ("converged", _int), ("rel_res", _d),
+                ("res_hist", ctypes.POINTER(_d)), ("alpha", ctypes.POINTER(_d)),
+                ("beta", ctypes.POINTER(_d)), ("t_solve_ms", _d)]
+
+
+SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc_quad_points",
+           "lorpc_rhs_assemble", "lorpc_operator_apply", "lorpc_lor_assemble", "lorpc_lor_destroy",
+           "lorpc_schwarz_setup", "lorpc_prec_destroy", "lorpc_precond_apply",
+           "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
+           "lorpc_launch_count", "lorpc_last_error"]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.lorpc_last_error.restype = ctypes.c_char_p
+        L.lorpc_mesh_create.argtypes = [ctypes.POINTER(MeshDesc), _vp, _vp, ctypes.POINTER(_vp)]
+        L.lorpc_mesh_destroy.argtypes = [_vp]
+        L.lorpc_mesh_sizes.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
+        L.lorpc_quad_points.argtypes = [_vp, _vp, _vp, _vp]
+        L.lorpc_rhs_assemble.argtypes = [_vp, _vp, _vp, _vp, _vp]
+        L.lorpc_operator_apply.argtypes = [_vp, _vp, _vp, _vp]
+        L.lorpc_lor_assemble.argtypes = [_vp, _vp, ctypes.POINTER(_vp)]
+        L.lorpc_lor_destroy.argtypes = [_vp]
+        L.lorpc_schwarz_setup.argtypes = [_vp, ctypes.POINTER(SchwarzDesc), _vp, ctypes.POINTER(_vp)]
+        L.lorpc_prec_destroy.argtypes = [_vp]
+        L.lorpc_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
+        L.lorpc_prec_export_ordering.argtypes = [_vp, _ll, _int, ctypes.POINTER(_int), ctypes.POINTER(_int)]
+        L.lorpc_prec_info.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_int)]
+        L.lorpc_pcg_solve.argtypes = [_vp, _vp, _vp, _vp, _d, _int, ctypes.POINTER(PcgReport), _vp]
+        L.lorpc_pcg_solve_host.argtypes = [_vp, _vp, _vp, _vp, _d, _int, ctypes.POINTER(PcgReport), _vp]
+        L.lorpc_launch_count.restype = _ll
+        L.lorpc_launch_count.argtypes = [_int]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise LorpcError(rc, lib().lorpc_last_error().decode())
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous(), \
+        "device vectors must be contiguous CUDA float64 tensors"
+    return t.data_ptr()
+
+
+def launch_count(reset=False):
+    return lib().lorpc_launch_count(1 if reset else 0)
+
+
+class Mesh:
+    """lorpc_mesh: Cartesian topology of multilinear tensor-product elements."""
+
+    def __init__(self, dim, n, p, vertices, disc=0, eta=0.0, stream=None):
+        n = list(n) + [1] * (3 - len(n))
+        self.desc = MeshDesc(dim, (_int * 3)(*n[:3]), p, disc, float(eta))
+        V = np.ascontiguousarray(vertices, dtype=np.float64)
+        h = _vp()
+        _check(lib().lorpc_mesh_create(ctypes.byref(self.desc), V.ctypes.data, _stream(stream), ctypes.byref(h)))
+        self.h = h
+        self.dim, self.p, self.disc = dim, p, disc
+        a, b, c = _ll(), _ll(), _ll()
+        _check(lib().lorpc_mesh_sizes(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        self.n_dof, self.n_quad, self.n_bface_quad = a.value, b.value, c.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lorpc_mesh_destroy(self.h)
+            self.h = None
+
+    def quad_points(self, xq=None, xbq=None, stream=None):
+        _check(lib().lorpc_quad_points(self.h, _dptr(xq), _dptr(xbq), _stream(stream)))
+
+    def rhs_assemble(self, fq, gq, b, stream=None):
+        _check(lib().lorpc_rhs_assemble(self.h, _dptr(fq), _dptr(gq), _dptr(b), _stream(stream)))
+
+    def apply(self, x, y, stream=None):
+        _check(lib().lorpc_operator_apply(self.h, _dptr(x), _dptr(y), _stream(stream)))
+
+
+class Lor:
+    """lorpc_lor: K_h on the GLL-refined mesh and the element-structured hierarchy."""
+
+    def __init__(self, mesh, stream=None):
+        self.mesh = mesh
+        h = _vp()
+        _check(lib().lorpc_lor_assemble(mesh.h, _stream(stream), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lorpc_lor_destroy(self.h)
+            self.h = None
+
+
+PATCH_KIND = {"vertex": 0, "star": 1}
+ORDERING = {"mdf": 0, "natural": 1}
+COARSE = {"gmg": 0, "none": 1}
+
+
+class Prec:
+    """lorpc_prec: additive Schwarz B (eq:as) or B_DG (eq:dg-as)."""
+
+    def __init__(self, lor, patch_kind="vertex", ordering="mdf", coarse="gmg", stream=None):
+        self.lor = lor
+        self.mesh = lor.mesh
+        self.desc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], COARSE[coarse])
+        h = _vp()
+        _check(lib().lorpc_schwarz_setup(lor.h, ctypes.byref(self.desc), _stream(stream), ctypes.byref(h)))
+        self.h = h
+        J, L = _ll(), _int()
+        _check(lib().lorpc_prec_info(self.h, ctypes.byref(J), ctypes.byref(L)))
+        self.n_patches, self.n_levels = J.value, L.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lorpc_prec_destroy(self.h)
+            self.h = None
+
+    def apply(self, r, z, stream=None):
+        _check(lib().lorpc_precond_apply(self.h, _dptr(r), _dptr(z), _stream(stream)))
+
+    def ordering(self, patch, level, cap=1024):
+        buf = (_int * cap)()
+        n = _int(cap)
+        _check(lib().lorpc_prec_export_ordering(self.h, patch, level, buf, ctypes.byref(n)))
+        return np.array(buf[:n.value], dtype=np.int64)
+
+
+def _report(rep, maxit, keep):
+    return {"iters": rep.iters, "converged": bool(rep.converged), "rel_res": rep.rel_res,
+            "t_solve_ms": rep.t_solve_ms,
+            "res": keep[0][:rep.iters + 1].copy(), "alpha": keep[1][:rep.iters].copy(),
+            "beta": keep[2][:max(rep.iters - 1, 0)].copy()}
+
+
+def _mkrep(maxit):
+    keep = (np.zeros(maxit + 1), np.zeros(maxit), np.zeros(maxit))
+    rep = PcgReport(0, 0, 0.0, keep[0].ctypes.data_as(ctypes.POINTER(_d)),
+                    keep[1].ctypes.data_as(ctypes.POINTER(_d)), keep[2].ctypes.data_as(ctypes.POINTER(_d)), 0.0)
+    return rep, keep
+
+
+def pcg_solve(mesh, prec, b, x, rtol, maxit=2000, stream=None, allow_not_converged=False):
+    rep, keep = _mkrep(maxit)
+    rc = lib().lorpc_pcg_solve(mesh.h, prec.h, _dptr(b), _dptr(x), float(rtol), int(maxit), ctypes.byref(rep),
+                               _stream(stream))
+    if rc != 0 and not (allow_not_converged and rc == 6):
+        _check(rc)
+    return _report(rep, maxit, keep)
+
+
+def pcg_solve_host(mesh, prec, b_host, x_host, rtol, maxit=2000, stream=None):
+    """End-to-end solve through the C ABI with host buffers (H2D / D2H inside the call)."""
+    rep, keep = _mkrep(maxit)
+    b_host = np.ascontiguousarray(b_host, dtype=np.float64)
+    assert x_host.dtype == np.float64 and x_host.flags.c_contiguous
+    _check(lib().lorpc_pcg_solve_host(mesh.h, prec.h, b_host.ctypes.data, x_host.ctypes.data, float(rtol),
+                                      int(maxit), ctypes.byref(rep), _stream(stream)))
+    return _report(rep, maxit, keep)

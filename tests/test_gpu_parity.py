@@ -1,0 +1,209 @@
+"""GPU-vs-oracle parity through the C ABI (north_star: relative 1e-11 per
+operator / preconditioner apply, PCG iterations within +-1).
+
+Inputs come only from workloads/ (seeded); expected values only from oracle/.
+Sizes span several elements / patches and clipped boundary patches; the
+full-size configs are checked on sampled outputs (tests marked slow on CPU side
+are not involved: everything here needs the GPU).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import (get_config, parity_vector, random_free_rhs, rhs_function, small_config,
+                       vertices)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1908_07071_b200 import lorpc
+    return lorpc
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+CASES = {
+    "C1": get_config("C1"),
+    "C2s": small_config("C2", (6, 5)),
+    "C2p3": small_config("C2", (5, 4), p=3),
+    "C3s": small_config("C3", (3, 4, 3)),
+    "C3p2": small_config("C3", (4, 3, 3), p=2),
+    "C5s": small_config("C5", (4, 3, 5)),
+    "C5p5": small_config("C5", (3, 3, 3), p=5),
+}
+
+
+def gpu_problem(L, cfg):
+    V = vertices(cfg)
+    return L.Mesh(cfg.dim, cfg.n, cfg.p, V)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_operator_parity(L, name):
+    cfg = CASES[name]
+    mesh = gpu_problem(L, cfg)
+    P = O.Problem.from_config(cfg)
+    x = parity_vector(P.ndof)
+    y = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.apply(dev(x), y)
+    yo = P.apply(x)
+    yg = y.cpu().numpy()
+    assert rel(yg, yo) <= TOL
+    assert np.abs(yg - yo).max() <= TOL * np.abs(yo).max()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C5s"])
+def test_rhs_parity(L, name):
+    cfg = CASES[name]
+    if cfg.rhs == "randn":
+        pytest.skip("C5 RHS is a random vector")
+    mesh = gpu_problem(L, cfg)
+    xq = torch.empty(mesh.n_quad * cfg.dim, dtype=torch.float64, device="cuda")
+    mesh.quad_points(xq)
+    P = O.Problem.from_config(cfg)
+    Xo = P.quad_points()
+    assert np.abs(xq.cpu().numpy().reshape(-1, cfg.dim) - Xo).max() < 1e-14
+    fq = dev(rhs_function(cfg, xq.cpu().numpy().reshape(-1, cfg.dim)))
+    b = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.rhs_assemble(fq, None, b)
+    bo = P.rhs(rhs_function(cfg, Xo))
+    assert rel(b.cpu().numpy(), bo) <= TOL
+
+
+def _setup_both(L, cfg, ordering="mdf", coarse="gmg"):
+    mesh = gpu_problem(L, cfg)
+    lor = L.Lor(mesh)
+    prec = L.Prec(lor, patch_kind=cfg.patch_kind, ordering=ordering, coarse=coarse)
+    P = O.Problem.from_config(cfg)
+    P.schwarz_setup(cfg.patch_kind, ordering, coarse)
+    return mesh, lor, prec, P
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_orderings_match_oracle(L, name):
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg)
+    assert prec.n_patches == P.npatches() and prec.n_levels == P.nlevels()
+    rng = np.random.default_rng(7)
+    pts = np.unique(np.concatenate([[0, prec.n_patches - 1, prec.n_patches // 2],
+                                    rng.integers(0, prec.n_patches, 12)]))
+    mism = 0
+    for j in pts:
+        for l in range(prec.n_levels - 1):   # the coarsest level is an exact solve (reading c8)
+            og = prec.ordering(int(j), l)
+            oo = P.patch_ordering(int(j), l)
+            if not np.array_equal(og, oo):
+                mism += 1
+    assert mism == 0
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("ordering", ["mdf", "natural"])
+def test_precond_parity(L, name, ordering):
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg, ordering=ordering)
+    r = parity_vector(P.ndof, seed=43)
+    X = P.node_coords()
+    free = np.all((X > 1e-12) & (X < 1 - 1e-12), axis=1)
+    r[~free] = 0.0
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    zo = P.precond(r)
+    zg = z.cpu().numpy()
+    assert rel(zg, zo) <= TOL, rel(zg, zo)
+
+
+@pytest.mark.parametrize("name", ["C2s", "C3s"])
+def test_precond_parity_no_coarse(L, name):
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg, coarse="none")
+    r = parity_vector(P.ndof, seed=44)
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    assert rel(z.cpu().numpy(), P.precond(r)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C5s"])
+def test_pcg_parity(L, name):
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg)
+    if cfg.rhs == "randn":
+        bo = random_free_rhs(cfg)
+    else:
+        bo = P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, cfg.tol)
+    xo, ro = P.pcg(bo, cfg.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 1
+    assert rep["converged"] and rep["rel_res"] <= cfg.tol
+    kg = O.lanczos_kappa(rep["alpha"], rep["beta"])
+    ko = O.lanczos_kappa(ro["alpha"], ro["beta"])
+    assert abs(kg - ko) <= 1e-6 * ko
+    assert rel(x.cpu().numpy(), xo) <= 100 * cfg.tol
+
+
+def test_pcg_host_buffers(L):
+    cfg = CASES["C2s"]
+    mesh, lor, prec, P = _setup_both(L, cfg)
+    bo = P.rhs(rhs_function(cfg, P.quad_points()))
+    xh = np.zeros(P.ndof)
+    rep = L.pcg_solve_host(mesh, prec, bo, xh, cfg.tol)
+    xo, ro = P.pcg(bo, cfg.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 1 and rel(xh, xo) <= 100 * cfg.tol
+
+
+def test_errors_are_reported(L):
+    with pytest.raises(L.LorpcError):
+        L.Mesh(2, (2, 2), 0, np.zeros((9, 2)))
+    V = vertices(small_config("C1", (2, 2)))
+    V[4] = V[0] + np.array([2.0, 2.0])  # fold the mesh: inverted elements
+    with pytest.raises(L.LorpcError) as e:
+        L.Mesh(2, (2, 2), 3, V)
+    assert e.value.code == 3
+
+
+# ---------------------------------------------------------------- full sizes
+def test_c2_full_pcg(L):
+    cfg = get_config("C2")
+    mesh, lor, prec, P = _setup_both(L, cfg)
+    bo = P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, cfg.tol)
+    xo, ro = P.pcg(bo, cfg.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 1
+    assert rel(x.cpu().numpy(), xo) <= 100 * cfg.tol
+    r = parity_vector(P.ndof, seed=45)
+    z = torch.empty_like(x)
+    prec.apply(dev(r), z)
+    assert rel(z.cpu().numpy(), P.precond(r)) <= TOL
+    y = torch.empty_like(x)
+    mesh.apply(dev(r), y)
+    assert rel(y.cpu().numpy(), P.apply(r)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_full_size_operator_sampled_rows(L, name):
+    cfg = get_config(name)
+    mesh = gpu_problem(L, cfg)
+    x = parity_vector(mesh.n_dof)
+    y = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.apply(dev(x), y)
+    P = O.Problem.from_config(cfg)
+    rng = np.random.default_rng(11)
+    rows = np.unique(np.concatenate([rng.integers(0, mesh.n_dof, 400), [0, mesh.n_dof - 1, mesh.n_dof // 2]]))
+    yo = P.apply_rows(x, rows)
+    yg = y.cpu().numpy()[rows]
+    assert np.abs(yg - yo).max() <= TOL * max(np.abs(yo).max(), 1.0)
