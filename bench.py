@@ -1,0 +1,282 @@
+#!/usr/bin/env python
+"""Benchmark: PCG DOFs x iterations / s (sum-factorised apply + LOR Schwarz), FP64.
+
+One "step" = one complete PCG solve (x_0 = 0 to the config tolerance) of the
+headline workload, i.e. one pass of every hot-path row (operator apply,
+patch restriction, patch V-cycles, coarse correction, Schwarz sum, PCG vector
+updates) per iteration; setup (geometry, LOR, MDF/ILU factorisation) is done
+once before the timed region.  value = n_dof x iterations x steps / time, summed
+over ranks.  See DESIGN.md §Measurement.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl lorpc|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HEADLINE = "C5"
+METRIC = "PCG DOFs×iters/s (sum-fact apply + LOR Schwarz), FP64, % HBM roofline"
+UNIT = "DOF-iters/s"
+# Oracle bounded sample for the CPU baseline / reference arm: same recipe, smaller mesh.
+CPU_SAMPLE = {"C1": (4, 4), "C2": (48, 48), "C3": (12, 12, 12), "C5": (16, 16, 16)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=HEADLINE)
+    ap.add_argument("--impl", default="lorpc", choices=["lorpc", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.path = os.path.join("/tmp", f"lorpc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            t = [v.strip() for v in line.split(",")]
+            if len(t) < 7:
+                continue
+            try:
+                sm.append(float(t[0]))
+                mx = max(mx, float(t[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, t[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(cfg_name, reps=1):
+    """Time the oracle (test infrastructure, never tuned) on a bounded sample of the
+    headline workload: same recipe, smaller mesh; full PCG solve, setup excluded."""
+    import oracle as O
+    from workloads import random_free_rhs, rhs_function, small_config
+    cfg = small_config(cfg_name, CPU_SAMPLE[cfg_name])
+    P = O.Problem.from_config(cfg)
+    b = random_free_rhs(cfg) if cfg.rhs == "randn" else P.rhs(rhs_function(cfg, P.quad_points()))
+    P.schwarz_setup(cfg.patch_kind, "mdf", "gmg")
+    P.apply(b)  # element-matrix cache built outside the timed region (setup)
+    t = 0.0
+    iters = 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, rep = P.pcg(b, cfg.tol)
+        t += time.perf_counter() - t0
+        iters += rep["iters"]
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    return {"value": P.ndof * iters / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.name}: {cfg_name} recipe (p={cfg.p}, same perturbation/seeds/RHS kind) on "
+                      f"{'x'.join(map(str, cfg.n))} elements, n_dof={P.ndof}, full PCG solve to tol={cfg.tol} "
+                      f"({iters // reps} iterations), setup excluded, {reps} solve(s), {t:.1f} s"}, t
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        oracle_sample(args.config)
+    vals, ts = [], []
+    for _ in range(args.steps):
+        cb, t = oracle_sample(args.config)
+        vals.append(cb["value"])
+        ts.append(t)
+    value = statistics.mean(vals)
+    cb["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(ts),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cb["sample"], "parallelism": "host OpenMP"},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_lorpc(args):
+    import numpy as np
+    import torch
+    from paper_1908_07071_b200 import build as B
+    from workloads import get_config, random_free_rhs, rhs_function, vertices
+
+    rank, world, local = dist_env()
+    if not os.path.exists(os.path.join(ROOT, "paper_1908_07071_b200", "liblorpc.so")):
+        B.build()
+    from paper_1908_07071_b200 import lorpc as L
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = get_config(args.config)
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, vertices(cfg))
+    lor = L.Lor(mesh)
+    prec = L.Prec(lor, patch_kind=cfg.patch_kind)
+    if cfg.rhs == "randn":
+        b_host = random_free_rhs(cfg)
+        b = torch.from_numpy(b_host).to(dev)
+    else:
+        xq = torch.empty(mesh.n_quad * cfg.dim, dtype=torch.float64, device=dev)
+        mesh.quad_points(xq)
+        fq = torch.from_numpy(rhs_function(cfg, xq.cpu().numpy().reshape(-1, cfg.dim))).to(dev)
+        b = torch.empty(mesh.n_dof, dtype=torch.float64, device=dev)
+        mesh.rhs_assemble(fq, None, b)
+        b_host = b.cpu().numpy()
+    x = torch.empty_like(b)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        L.pcg_solve(mesh, prec, b, x, cfg.tol, cfg.maxit)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    L.launch_count(reset=True)
+    prec.profile(True)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    e0.record(s)
+    for _ in range(args.steps):
+        rep = L.pcg_solve(mesh, prec, b, x, cfg.tol, cfg.maxit)
+        iters.append(rep["iters"])
+    e1.record(s)
+    torch.cuda.synchronize()
+    launches = L.launch_count()
+    vc_ms, vc_n = prec.profile_read()
+    prec.profile(False)
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    work = mesh.n_dof * sum(iters) * world
+    value = work / (ms * 1e-3)
+
+    # end to end: host (pinned) b in, host x out, through lorpc_pcg_solve_host
+    bh = torch.from_numpy(b_host).pin_memory()
+    xh = torch.empty(mesh.n_dof, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    te = time.perf_counter()
+    it_e2e = 0
+    for _ in range(args.steps):
+        rep = L.pcg_solve_host(mesh, prec, bh.numpy(), xh.numpy(), cfg.tol, cfg.maxit)
+        it_e2e += rep["iters"]
+    torch.cuda.synchronize()
+    te = time.perf_counter() - te
+    if dist:
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    e2e = mesh.n_dof * it_e2e * world / te
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    # roofline of the dominant kernel: patch V-cycle (algorithmic bytes)
+    fv, lvl_nodes, cnodes = prec.byte_model()
+    half = 14 if cfg.dim == 3 else 5
+    vc_bytes = 8 * fv + 8 * half * sum(lvl_nodes) + 16 * mesh.n_dof
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    per_launch_ms = vc_ms / max(vc_n, 1)
+    achieved = vc_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("k_vcycle_bytes_per_launch")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded workloads/ generators)",
+            "config": {"workload": f"{cfg.name}: {cfg.dim}D {cfg.disc.upper()} {'x'.join(map(str, cfg.n))} "
+                                   f"p={cfg.p}, perturb={cfg.perturb}h, {cfg.patch_kind} patches, "
+                                   f"MDF-ILU(0) V(1,1), GMG R_0, tol={cfg.tol}",
+                       "n_dof": mesh.n_dof, "pcg_iters_per_solve": iters[0], "n_patches": prec.n_patches,
+                       "setup_s": round(t_setup, 3), "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (working set >> 126 MB)" if mesh.n_dof > 4_000_000
+                       else "L2-resident working set (no flush; latency case)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_vcycle (patch V-cycle)",
+                         "algorithmic_bytes_per_launch": vc_bytes, "launch_ms": per_launch_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * mesh.n_dof,
+                    "d2h_bytes_per_step": 8 * mesh.n_dof},
+            "gpu_launches": launches, "clocks": ck}
+    if world == 1 and not args.no_cpu_baseline:
+        cb, _ = oracle_sample(args.config)
+        line["cpu_baseline"] = cb
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lorpc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

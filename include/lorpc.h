@@ -132,6 +132,17 @@ int lorpc_precond_apply(const lorpc_prec* b, const double* r_dev, double* z_dev,
 int lorpc_prec_export_ordering(const lorpc_prec* b, long long patch, int level, int* perm_host, int* n);
 /* Number of patches and hierarchy levels. */
 int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels);
+/* Algorithmic byte-model inputs: factor_values = sum over
+ * patches and levels of (free nodes + stencil edges), i.e. the L and D values of
+ * every M_l = L D L^T; level_nodes[l] = nodes of the level-l grid (l < n_levels),
+ * coarse_nodes = nodes of all R_0 GMG levels. */
+int lorpc_prec_bytes(const lorpc_prec* b, long long* factor_values, long long* level_nodes, long long* coarse_nodes);
+/* Live timing of the patch V-cycle kernel (the dominant kernel): enable = 1
+ * starts recording a CUDA event pair around every launch on the apply stream
+ * (up to 4096 launches), enable = 0 stops; lorpc_prec_profile_read synchronizes
+ * and returns the summed device time (ms) and launch count, then resets. */
+int lorpc_prec_profile(lorpc_prec* b, int enable);
+int lorpc_prec_profile_read(lorpc_prec* b, double* ms, long long* launches);
 
 /* ---- PCG (a10) ------------------------------------------------------------------ */
 /* Preconditioned conjugate gradients (reading c12): x_0 = 0,

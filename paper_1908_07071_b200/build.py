@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblorpc.so")
-SOURCES = ["basis.cpp", "mesh.cu", "operator.cu", "lor.cu", "schwarz.cu", "pcg.cu", "dg.cu", "api.cu"]
+SOURCES = ["basis.cpp", "mesh.cu", "operator.cu", "lor.cu", "schwarz.cu", "vcycle.cu", "pcg.cu", "dg.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
@@ -14,7 +14,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 def build(force=False, verbose=False):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in ("common.h", "device.cuh")] + \
+    deps = srcs + [os.path.join(CSRC, h) for h in ("common.h", "device.cuh", "patch.cuh")] + \
         [os.path.join(HERE, "..", "include", "lorpc.h")]
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in deps):
         return OUT
@@ -26,7 +26,7 @@ def build(force=False, verbose=False):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if os.path.exists(obj) and not force and os.path.getmtime(obj) >= max(
-                [os.path.getmtime(src)] + [os.path.getmtime(os.path.join(CSRC, h)) for h in ("common.h", "device.cuh")]
+                [os.path.getmtime(src)] + [os.path.getmtime(os.path.join(CSRC, h)) for h in ("common.h", "device.cuh", "patch.cuh")]
                 + [os.path.getmtime(os.path.join(HERE, "..", "include", "lorpc.h"))]):
             continue
         cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]

@@ -160,11 +160,12 @@ void lorpc_prec_destroy(lorpc_prec* b) {
     if (i > 0) dfree(b->Ac[i]);
     dfree(b->dl1[i]); dfree(b->cr[i]); dfree(b->cz[i]); dfree(b->cs[i]);
   }
-  dfree(b->coarse_chol); dfree(b->rcg); dfree(b->zcg); dfree(b->xb);
+  dfree(b->coarse_chol); dfree(b->rcg); dfree(b->zcg); dfree(b->xb); dfree(b->wtab);
   dfree(b->r); dfree(b->z); dfree(b->pv); dfree(b->qv); dfree(b->scal); dfree(b->part);
   if (b->hostpin) cudaFreeHost(b->hostpin);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
+  for (auto& e : b->prof_ev) cudaEventDestroy(e);
   delete b;
 }
 
@@ -183,6 +184,44 @@ int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels) {
   if (!b) return fail(LORPC_ERR_ARG, "prec_info: NULL");
   if (n_patches) *n_patches = b->J;
   if (n_levels) *n_levels = b->L;
+  return LORPC_OK;
+}
+
+int lorpc_prec_bytes(const lorpc_prec* b, long long* factor_values, long long* level_nodes, long long* coarse_nodes) {
+  if (!b) return fail(LORPC_ERR_ARG, "prec_bytes: NULL");
+  if (factor_values) *factor_values = b->factor_values;
+  if (level_nodes)
+    for (int l = 0; l < b->L; ++l) level_nodes[l] = b->lor->Nl[l];
+  if (coarse_nodes) {
+    long long c = 0;
+    for (int l = 0; l < b->nc; ++l) c += b->cN[l];
+    *coarse_nodes = c;
+  }
+  return LORPC_OK;
+}
+
+int lorpc_prec_profile(lorpc_prec* b, int enable) {
+  if (!b) return fail(LORPC_ERR_ARG, "prec_profile: NULL");
+  if (enable && b->prof_ev.empty()) {
+    b->prof_ev.resize(8192);
+    for (auto& e : b->prof_ev) LORPC_CUDA(cudaEventCreate(&e));
+  }
+  b->prof_on = enable != 0;
+  return LORPC_OK;
+}
+
+int lorpc_prec_profile_read(lorpc_prec* b, double* ms, long long* launches) {
+  if (!b || !ms || !launches) return fail(LORPC_ERR_ARG, "prec_profile_read: NULL");
+  double acc = 0.0;
+  for (int i = 0; i < b->prof_n; ++i) {
+    LORPC_CUDA(cudaEventSynchronize(b->prof_ev[2 * i + 1]));
+    float t = 0.f;
+    LORPC_CUDA(cudaEventElapsedTime(&t, b->prof_ev[2 * i], b->prof_ev[2 * i + 1]));
+    acc += t;
+  }
+  *ms = acc;
+  *launches = b->prof_n;
+  b->prof_n = 0;
   return LORPC_OK;
 }
 

@@ -109,6 +109,12 @@ struct lorpc_prec {
   long long* recoff = nullptr;      // [J][L] byte offsets
   std::vector<long long> recoff_h;
   long long rec_bytes = 0;
+  long long rec_max = 0;            // largest per-patch record span (bytes)
+  // separable patch restriction tables: level l -> l+1, e elements along an axis
+  double* wtab = nullptr;
+  int woff[lorpc::MAXL][4], wfe[lorpc::MAXL][4], wce[lorpc::MAXL][4];
+  int scratch_doubles = 0;          // per-patch transfer scratch (V-cycle kernel)
+  int lanes = 8;                    // lanes per patch in the V-cycle kernel
   // coarse space (R_0)
   int nc = 0;                       // GMG levels
   int cn[lorpc::MAXC][3];           // vertices per axis
@@ -131,6 +137,12 @@ struct lorpc_prec {
   double* xb = nullptr;             // host-buffer solve staging (b, x)
   cudaStream_t aux = nullptr;       // second stream (coarse chain)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // live timing of the dominant kernel (patch V-cycle), lorpc_prec_profile()
+  bool prof_on = false;
+  int prof_n = 0;
+  std::vector<cudaEvent_t> prof_ev;
+  // algorithmic byte model inputs
+  long long factor_values = 0;      // sum over patch-levels of (n + nL)
 };
 
 namespace lorpc {

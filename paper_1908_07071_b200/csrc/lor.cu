@@ -99,7 +99,7 @@ __global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __re
     }
   }
 #pragma unroll
-  for (int d = 0; d < ND; ++d) A[(long long)d * Ntot + g] = row[d];
+  for (int d = 0; d < ND; ++d) A[g * ND + d] = row[d];
 }
 
 // weight of coarse 1D index ic in the interpolation row of fine 1D index f
@@ -164,7 +164,7 @@ __global__ void k_galerkin(const double* __restrict__ Af, double* __restrict__ A
           const int b[3] = {fx + dir_dx(d), fy + dir_dy(d), fz + (DIM == 3 ? dir_dz(d) : 0)};
           if (b[0] < 0 || b[0] >= Nfx || b[1] < 0 || b[1] >= Nfy) continue;
           if (DIM == 3 && (b[2] < 0 || b[2] >= Nfz)) continue;
-          const double av = Af[(long long)d * NfT + a];
+          const double av = Af[a * ND + d];
           if (av == 0.0) continue;
           int c0[3], c1[3]; double w0[3], w1[3];
 #pragma unroll
@@ -195,7 +195,7 @@ __global__ void k_galerkin(const double* __restrict__ Af, double* __restrict__ A
     }
   }
 #pragma unroll
-  for (int d = 0; d < ND; ++d) Ac[(long long)d * NcT + I] = row[d];
+  for (int d = 0; d < ND; ++d) Ac[I * ND + d] = row[d];
 }
 
 static Transfer1D make_transfer(const double* xi, const std::vector<int>& fine, const std::vector<int>& coarse) {

@@ -1,0 +1,116 @@
+// Patch geometry, ILU record layout and grid helpers shared by the Schwarz
+// setup (schwarz.cu) and apply (vcycle.cu) translation units.
+#pragma once
+#include "device.cuh"
+
+namespace lorpc {
+
+// ------------------------------------------------------------------ patch geometry
+struct PatchGeom {
+  int d, kind;          // kind 0 vertex, 1 star
+  int n[3];             // elements per axis
+  int ml[MAXL];         // nodes per element per axis at each level
+  int Nax[MAXL][3];     // level grid per axis
+  int L;
+};
+
+__host__ __device__ __forceinline__ void patch_elems(const PatchGeom& G, long long j, int* elo, int* ehi) {
+  if (G.kind == 0) {
+    const long long nv0 = G.n[0] + 1, nv1 = G.n[1] + 1;
+    const int v[3] = {(int)(j % nv0), (int)((j / nv0) % nv1), (int)(j / (nv0 * nv1))};
+    for (int k = 0; k < 3; ++k) {
+      if (k >= G.d) { elo[k] = ehi[k] = 0; continue; }
+      elo[k] = v[k] - 1 < 0 ? 0 : v[k] - 1;
+      ehi[k] = v[k] < G.n[k] - 1 ? v[k] : G.n[k] - 1;
+    }
+  } else {
+    const int e[3] = {(int)(j % G.n[0]), (int)((j / G.n[0]) % G.n[1]), (int)(j / ((long long)G.n[0] * G.n[1]))};
+    for (int k = 0; k < 3; ++k) {
+      if (k >= G.d) { elo[k] = ehi[k] = 0; continue; }
+      elo[k] = e[k] - 1 < 0 ? 0 : e[k] - 1;
+      ehi[k] = e[k] + 1 < G.n[k] - 1 ? e[k] + 1 : G.n[k] - 1;
+    }
+  }
+}
+// free node box at level l: first free node lo[k] (level-global), extent ext[k]
+__host__ __device__ __forceinline__ void patch_box(const PatchGeom& G, long long j, int l, int* lo, int* ext) {
+  int elo[3], ehi[3];
+  patch_elems(G, j, elo, ehi);
+  const int m = G.ml[l];
+  for (int k = 0; k < 3; ++k) {
+    if (k >= G.d) { lo[k] = 0; ext[k] = 1; continue; }
+    lo[k] = elo[k] * (m - 1) + 1;
+    ext[k] = (ehi[k] - elo[k] + 1) * (m - 1) - 1;
+  }
+}
+__host__ __device__ __forceinline__ long long num_edges(int d, const int* ext) {
+  // half-stencil directions: lexicographically positive offsets
+  long long s = 0;
+  for (int dz = (d == 3 ? -1 : 0); dz <= (d == 3 ? 1 : 0); ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const bool pos = dz > 0 || (dz == 0 && (dy > 0 || (dy == 0 && dx > 0)));
+        if (!pos) continue;
+        long long c = 1;
+        const int o[3] = {dx, dy, dz};
+        for (int k = 0; k < d; ++k) { int v = ext[k] - (o[k] < 0 ? -o[k] : o[k]); c *= v > 0 ? v : 0; }
+        s += c;
+      }
+  return s;
+}
+__host__ __device__ __forceinline__ long long a8(long long b) { return (b + 7) & ~7ll; }
+// Per patch-level ILU record.  Rows are stored in schedule order t (DAG levels
+// of the triangular solves, ties in elimination order):
+//   D[n]      pivots (natural index)
+//   L[nL]     lower entries L_ij of row sched[t], rows consecutive (forward sweep)
+//   fnbr[nL]  natural index j of each L entry
+//   frow[n+1] row pointers into L / fnbr
+//   bent[nL]  backward entries of row sched[t]: (k | pos << 16) with L[pos] = L_ki
+//   brow[n+1] row pointers into bent
+//   sched[n], lptr[n+1] (DAG level pointers), order[n] (elimination order)
+struct RecLayout { long long D, L, fnbr, frow, bent, brow, sched, lptr, order, total; };
+__host__ __device__ __forceinline__ RecLayout rec_layout(int n, long long nL) {
+  RecLayout R;
+  R.D = 16;
+  R.L = R.D + 8ll * n;
+  R.fnbr = R.L + 8ll * nL;
+  R.frow = R.fnbr + a8(2ll * nL);
+  R.bent = R.frow + a8(2ll * (n + 1));
+  R.brow = R.bent + a8(4ll * nL);
+  R.sched = R.brow + a8(2ll * (n + 1));
+  R.lptr = R.sched + a8(2ll * n);
+  R.order = R.lptr + a8(2ll * (n + 1));
+  R.total = (R.order + 2ll * n + 15) & ~15ll;  // 16-byte aligned patch records
+  return R;
+}
+
+
+template <int DIM>
+__device__ __forceinline__ int doff(int d, int ex, int ey) {
+  return dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
+}
+
+template <int DIM>
+__device__ __forceinline__ bool interior_of(long long g, int3 Nv, int* c) {
+  c[0] = (int)(g % Nv.x); c[1] = (int)((g / Nv.x) % Nv.y); c[2] = (int)(g / ((long long)Nv.x * Nv.y));
+  bool in = c[0] > 0 && c[0] < Nv.x - 1 && c[1] > 0 && c[1] < Nv.y - 1;
+  if (DIM == 3) in = in && c[2] > 0 && c[2] < Nv.z - 1;
+  return in;
+}
+template <int DIM>
+__device__ __forceinline__ double stencil_apply(const double* A, const double* z, long long g, int3 Nv, long long NT) {
+  constexpr int ND = Dirs<DIM>::ND;
+  double acc = 0.0;
+  for (int d = 0; d < ND; ++d) {
+    const long long o = dir_dx(d) + (long long)Nv.x * (dir_dy(d) + (long long)Nv.y * (DIM == 3 ? dir_dz(d) : 0));
+    acc += A[g * ND + d] * z[g + o];
+  }
+  return acc;
+}
+// mode 0: z = r / d ; s = (later) ;  mode 1: s = r - A z ; mode 2: z += (r - A z)/d written to s then copied
+
+static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+static inline int3 i3(const int* a) { return make_int3(a[0], a[1], a[2]); }
+PatchGeom make_geom(const lorpc_prec* b);
+
+}  // namespace lorpc

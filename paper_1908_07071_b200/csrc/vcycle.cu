@@ -1,0 +1,594 @@
+// Schwarz apply: patch V-cycles (rows a5, a6, a8) and the coarse correction (a7).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "patch.cuh"
+
+namespace lorpc {
+
+// ------------------------------------------------------------------ coarse space R_0
+// P_0^T r: vertex v gathers the LOR nodes of its 2^d adjacent elements with the
+// multilinear hat weights in the GLL reference coordinate.
+template <int DIM>
+__global__ void k_restrict_vertex(const double* __restrict__ r, double* __restrict__ rc, int3 nv, int3 N, Basis1D bs) {
+  const long long NV = (long long)nv.x * nv.y * nv.z;
+  const long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (v >= NV) return;
+  const int vc[3] = {(int)(v % nv.x), (int)((v / nv.x) % nv.y), (int)(v / ((long long)nv.x * nv.y))};
+  const int Nn[3] = {N.x, N.y, N.z}, nvv[3] = {nv.x, nv.y, nv.z};
+  bool interior = true;
+  for (int k = 0; k < DIM; ++k) if (vc[k] == 0 || vc[k] == nvv[k] - 1) interior = false;
+  if (!interior) { rc[v] = 0.0; return; }
+  const int p = bs.p;
+  int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  for (int k = 0; k < DIM; ++k) { lo[k] = (vc[k] - 1) * p + 1; hi[k] = (vc[k] + 1) * p - 1; }
+  double acc = 0.0;
+  for (int gz = lo[2]; gz <= hi[2]; ++gz) {
+    double wz = 1.0;
+    if (DIM == 3) { const int t = gz - vc[2] * p; wz = t <= 0 ? bs.xi[t + p] : 1.0 - bs.xi[t]; }
+    for (int gy = lo[1]; gy <= hi[1]; ++gy) {
+      const int ty = gy - vc[1] * p;
+      const double wy = ty <= 0 ? bs.xi[ty + p] : 1.0 - bs.xi[ty];
+      for (int gx = lo[0]; gx <= hi[0]; ++gx) {
+        const int tx = gx - vc[0] * p;
+        const double wx = tx <= 0 ? bs.xi[tx + p] : 1.0 - bs.xi[tx];
+        acc += wx * wy * wz * r[gx + (long long)Nn[0] * (gy + (long long)Nn[1] * gz)];
+      }
+    }
+  }
+  rc[v] = acc;
+}
+
+// z += P_0 z_0, then z_D = 0
+template <int DIM>
+__global__ void k_prolong_vertex_add(const double* __restrict__ zc, double* __restrict__ z, int3 nv, int3 N, int3 n,
+                                     Basis1D bs) {
+  const long long NT = (long long)N.x * N.y * N.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  const int gc[3] = {(int)(g % N.x), (int)((g / N.x) % N.y), (int)(g / ((long long)N.x * N.y))};
+  const int Nn[3] = {N.x, N.y, N.z}, nn[3] = {n.x, n.y, n.z};
+  bool dir = false;
+  for (int k = 0; k < DIM; ++k) if (gc[k] == 0 || gc[k] == Nn[k] - 1) dir = true;
+  if (dir) { z[g] = 0.0; return; }
+  const int p = bs.p;
+  int v0[3] = {0, 0, 0};
+  double w0[3] = {1, 1, 1}, w1[3] = {0, 0, 0};
+  for (int k = 0; k < DIM; ++k) {
+    const int e = min(gc[k] / p, nn[k] - 1);
+    const int a = gc[k] - e * p;
+    v0[k] = e; w0[k] = 1.0 - bs.xi[a]; w1[k] = bs.xi[a];
+  }
+  double acc = 0.0;
+  for (int sel = 0; sel < (1 << DIM); ++sel) {
+    double w = 1.0;
+    int vv[3] = {0, 0, 0};
+    for (int k = 0; k < DIM; ++k) {
+      const int b = (sel >> k) & 1;
+      w *= b ? w1[k] : w0[k];
+      vv[k] = v0[k] + b;
+    }
+    if (w == 0.0) continue;
+    acc += w * zc[vv[0] + (long long)nv.x * (vv[1] + (long long)nv.y * vv[2])];
+  }
+  z[g] += acc;
+}
+
+// l1-Jacobi diagonal over interior columns of interior rows
+
+template <int DIM>
+__global__ void k_jacobi_pre(const double* __restrict__ r, const double* __restrict__ dl, double* __restrict__ z, int3 Nv) {
+  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  int c[3];
+  z[g] = interior_of<DIM>(g, Nv, c) ? r[g] / dl[g] : 0.0;
+}
+template <int DIM>
+__global__ void k_residual_grid(const double* __restrict__ A, const double* __restrict__ r, const double* __restrict__ z,
+                                double* __restrict__ s, int3 Nv) {
+  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  int c[3];
+  s[g] = interior_of<DIM>(g, Nv, c) ? r[g] - stencil_apply<DIM>(A, z, g, Nv, NT) : 0.0;
+}
+template <int DIM>
+__global__ void k_jacobi_post(const double* __restrict__ A, const double* __restrict__ r, const double* __restrict__ dl,
+                              const double* __restrict__ z, double* __restrict__ znew, int3 Nv) {
+  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  int c[3];
+  znew[g] = interior_of<DIM>(g, Nv, c) ? z[g] + (r[g] - stencil_apply<DIM>(A, z, g, Nv, NT)) / dl[g] : 0.0;
+}
+// rc = P^T s (2:1 vertex-centred): coarse I gathers fine 2I-1..2I+1 per axis with 1/2,1,1/2
+template <int DIM>
+__global__ void k_restrict_grid(const double* __restrict__ s, double* __restrict__ rc, int3 Nf, int3 Nc) {
+  const long long NT = (long long)Nc.x * Nc.y * Nc.z;
+  const long long I = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (I >= NT) return;
+  int c[3];
+  if (!interior_of<DIM>(I, Nc, c)) { rc[I] = 0.0; return; }
+  double acc = 0.0;
+  for (int oz = (DIM == 3 ? -1 : 0); oz <= (DIM == 3 ? 1 : 0); ++oz)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int ox = -1; ox <= 1; ++ox) {
+        const double w = (ox ? 0.5 : 1.0) * (oy ? 0.5 : 1.0) * (oz ? 0.5 : 1.0);
+        const long long f = (2 * c[0] + ox) + (long long)Nf.x * ((2 * c[1] + oy) + (long long)Nf.y * (DIM == 3 ? 2 * c[2] + oz : 0));
+        acc += w * s[f];
+      }
+  rc[I] = acc;
+}
+// z += P e (2:1 vertex-centred), interior fine nodes only
+template <int DIM>
+__global__ void k_prolong_grid_add(const double* __restrict__ e, double* __restrict__ z, int3 Nf, int3 Nc) {
+  const long long NT = (long long)Nf.x * Nf.y * Nf.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  int c[3];
+  if (!interior_of<DIM>(g, Nf, c)) return;
+  double acc = 0.0;
+  for (int sel = 0; sel < (1 << DIM); ++sel) {
+    double w = 1.0;
+    int cc[3] = {0, 0, 0};
+    bool ok = true;
+    for (int k = 0; k < DIM; ++k) {
+      const int b = (sel >> k) & 1;
+      if (c[k] % 2 == 0) { if (b) { ok = false; break; } cc[k] = c[k] / 2; }
+      else { cc[k] = c[k] / 2 + b; w *= 0.5; }
+    }
+    if (!ok) continue;
+    acc += w * e[cc[0] + (long long)Nc.x * (cc[1] + (long long)Nc.y * cc[2])];
+  }
+  z[g] += acc;
+}
+// coarsest GMG level: dense LDL^T over its interior nodes (one block)
+
+template <int DIM>
+__global__ void k_coarsest_solve(const double* __restrict__ F, const double* __restrict__ r, double* __restrict__ z,
+                                 int3 Nv, int nint) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
+  double x[64];
+  int idx = 0;
+  for (long long g = 0; g < NT; ++g) { int c[3]; if (interior_of<DIM>(g, Nv, c)) x[idx++] = r[g]; }
+  for (int i = 0; i < nint; ++i) {
+    double s = x[i];
+    for (int k = 0; k < i; ++k) s -= F[i * nint + k] * x[k];
+    x[i] = s / F[i * nint + i];
+  }
+  for (int i = nint - 1; i >= 0; --i) {
+    double s = x[i];
+    for (int k = i + 1; k < nint; ++k) s -= F[k * nint + i] * x[k];
+    x[i] = s / F[i * nint + i];
+  }
+  idx = 0;
+  for (long long g = 0; g < NT; ++g) { int c[3]; z[g] = interior_of<DIM>(g, Nv, c) ? x[idx++] : 0.0; }
+}
+
+
+// ------------------------------------------------------------------ patch V-cycle
+// Lane-group kernel: G lanes per patch, 32/G patches per warp (the level
+// schedules of MDF-ordered ILU(0) on 3D patches hold ~3-5 rows per DAG level,
+// so a full warp per patch left ~90% of the lanes idle; ncu r01).  Per patch the
+// shared memory holds the level vectors r_l, z_l, s_l and a transfer scratch;
+// the ILU records are read through L1/L2; the level operators A_l are read
+// row-major (AoS, 3^d contiguous doubles per node).
+struct VcParams {
+  PatchGeom G;
+  const double* A[MAXL];
+  const double* W;        // separable 1D restriction tables (host-built, see schwarz.cu)
+  int woff[MAXL][4];      // table offset for (level l -> l+1, elements along the axis 1..3)
+  int wfe[MAXL][4];       // fine extent of that table
+  int wce[MAXL][4];       // coarse extent
+  const char* rec;
+  const long long* recoff;
+  long long J;
+  int soff[MAXL];         // per-patch SMEM offsets (doubles) of [r | z | s] at level l
+  int nmax[MAXL];
+  int toff;               // transfer scratch offset
+  int roff;               // staged record offset (doubles), rec_doubles long
+  int rec_doubles;
+  int boff;               // mbarrier offset (doubles)
+  long long rec_total;
+  int patch_doubles;
+  const double* r;
+  double* z;
+};
+
+// v := M^{-1} v, M = L D L^T of one patch level (group-local lanes gl in [0,G))
+template <int G>
+__device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int gl) {
+  int n = 0, depth = 0, nL = 0;
+  if (act) { const int* h = (const int*)rec; n = h[0]; depth = h[1]; nL = h[2]; }
+  const int md = __reduce_max_sync(0xffffffffu, depth);
+  if (md == 0) return;
+  const RecLayout R = rec_layout(n, nL);
+  const double* D = (const double*)(rec + R.D);
+  const double* L = (const double*)(rec + R.L);
+  const uint16_t* fnbr = (const uint16_t*)(rec + R.fnbr);
+  const uint16_t* frow = (const uint16_t*)(rec + R.frow);
+  const uint32_t* bent = (const uint32_t*)(rec + R.bent);
+  const uint16_t* brow = (const uint16_t*)(rec + R.brow);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* lpt = (const uint16_t*)(rec + R.lptr);
+  for (int lv = 0; lv < md; ++lv) {
+    if (lv < depth) {
+      const int b = lpt[lv], e = lpt[lv + 1];
+      for (int t = b + gl; t < e; t += G) {
+        const int i = sch[t];
+        const int e0 = frow[t], e1 = frow[t + 1];
+        double a0 = v[i], a1 = 0.0;
+        int q = e0;
+        // batches of 4 independent (index, value, v) loads before the FMAs
+        for (; q + 4 <= e1; q += 4) {
+          const int n0 = fnbr[q], n1 = fnbr[q + 1], n2 = fnbr[q + 2], n3 = fnbr[q + 3];
+          const double l0 = L[q], l1 = L[q + 1], l2 = L[q + 2], l3 = L[q + 3];
+          const double v0 = v[n0], v1 = v[n1], v2 = v[n2], v3 = v[n3];
+          a0 -= l0 * v0; a1 += l1 * v1; a0 -= l2 * v2; a1 += l3 * v3;
+        }
+        for (; q < e1; ++q) a0 -= L[q] * v[fnbr[q]];
+        v[i] = a0 - a1;
+      }
+    }
+    __syncwarp();
+  }
+  for (int i = gl; i < n; i += G) v[i] = v[i] / D[i];
+  __syncwarp();
+  for (int lv = md - 1; lv >= 0; --lv) {
+    if (lv < depth) {
+      const int b = lpt[lv], e = lpt[lv + 1];
+      for (int t = b + gl; t < e; t += G) {
+        const int i = sch[t];
+        const int e0 = brow[t], e1 = brow[t + 1];
+        double a0 = v[i], a1 = 0.0;
+        int q = e0;
+        for (; q + 4 <= e1; q += 4) {
+          const uint32_t u0 = bent[q], u1 = bent[q + 1], u2 = bent[q + 2], u3 = bent[q + 3];
+          const double l0 = L[u0 >> 16], l1 = L[u1 >> 16], l2 = L[u2 >> 16], l3 = L[u3 >> 16];
+          const double v0 = v[u0 & 0xffffu], v1 = v[u1 & 0xffffu], v2 = v[u2 & 0xffffu], v3 = v[u3 & 0xffffu];
+          a0 -= l0 * v0; a1 += l1 * v1; a0 -= l2 * v2; a1 += l3 * v3;
+        }
+        for (; q < e1; ++q) { const uint32_t u0 = bent[q]; a0 -= L[u0 >> 16] * v[u0 & 0xffffu]; }
+        v[i] = a0 - a1;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// s = r - A_l z on the patch box (A_l row-major: ND contiguous doubles per node)
+template <int DIM, int G>
+__device__ __forceinline__ void residual_g(const double* __restrict__ A, long long Nx, long long Ny, const int* lo,
+                                           const int* ext, const double* r, const double* z, double* s, int n, int gl) {
+  constexpr int ND = Dirs<DIM>::ND;
+  const int ex = ext[0], ey = ext[1], ez = ext[2];
+  for (int i = gl; i < n; i += G) {
+    const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
+    const long long gi = (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0));
+    const double* Ar = A + gi * ND;
+    const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
+    double a0 = r[i], a1 = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const double zv = (em & (1u << d)) ? z[i + doff<DIM>(d, ex, ey)] : 0.0;
+      const double t2 = __ldg(Ar + d) * zv;
+      if (d & 1) a1 += t2; else a0 -= t2;
+    }
+    s[i] = a0 - a1;
+  }
+}
+
+template <int DIM, int G>
+__global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
+  constexpr int PPW = 32 / G;
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
+  const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (wg * PPW >= P.J) return;  // warp-uniform
+  const long long j = wg * PPW + grp;
+  const bool act = j < P.J;
+  double* W = sm + (long long)((threadIdx.x >> 5) * PPW + grp) * P.patch_doubles;
+  const int L = P.G.L;
+  int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
+  if (act) patch_elems(P.G, j, elo, ehi);
+  int ec[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) ec[k] = ehi[k] - elo[k] + 1;
+  auto box = [&](int l, int* lo, int* ext) {
+    const int m = P.G.ml[l];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= DIM) { lo[k] = 0; ext[k] = 1; continue; }
+      lo[k] = elo[k] * (m - 1) + 1;
+      ext[k] = act ? ec[k] * (m - 1) - 1 : 0;
+    }
+  };
+  auto rv = [&](int l) { return W + P.soff[l]; };
+  auto zv = [&](int l) { return W + P.soff[l] + P.nmax[l]; };
+  auto sv = [&](int l) { return W + P.soff[l] + 2 * P.nmax[l]; };
+  // ---- stage this patch's ILU records (all levels, contiguous, 16 B aligned) in
+  // shared memory with one TMA bulk copy (cp.async.bulk + mbarrier transaction count)
+  const long long rb0 = act ? P.recoff[j * L] : 0;
+  const long long rb1 = act ? ((j + 1 < P.J) ? P.recoff[(j + 1) * L] : P.rec_total) : 0;
+  char* srec = (char*)(W + P.roff);
+  {
+    uint64_t* bar = (uint64_t*)(W + P.boff);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bar);
+    const unsigned dst_s = (unsigned)__cvta_generic_to_shared(srec);
+    const unsigned bytes = (unsigned)(rb1 - rb0);
+    if (P.rec_doubles == 0) srec = (char*)(P.rec + rb0);   // records read through L1/L2
+    else if (act && gl == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
+          "l"(P.rec + rb0), "r"(bytes), "r"(bar_s)
+          : "memory");
+    }
+    __syncwarp();
+    if (act && P.rec_doubles > 0) {
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar_s)
+            : "memory");
+      }
+    }
+  }
+  auto recl = [&](int l) { return (const char*)srec + (act ? P.recoff[j * L + l] - rb0 : 0); };
+  double* T1 = W + P.toff;
+  // ---- gather r_j = I_j^T r (a5)
+  {
+    int lo[3], ext[3];
+    box(0, lo, ext);
+    const int n = ext[0] * ext[1] * ext[2];
+    const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+    double* r0 = rv(0);
+    for (int i = gl; i < n; i += G) {
+      const int ix = i % ext[0], iy = (i / ext[0]) % ext[1], iz = i / (ext[0] * ext[1]);
+      r0[i] = __ldg(P.r + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)));
+    }
+  }
+  __syncwarp();
+  // ---- downward leg: pre-smooth, residual, restrict (separable P^T)
+  for (int l = 0; l < L - 1; ++l) {
+    int lo[3], ext[3], clo[3], cext[3];
+    box(l, lo, ext);
+    box(l + 1, clo, cext);
+    const int n = ext[0] * ext[1] * ext[2];
+    double *r = rv(l), *z = zv(l), *s = sv(l);
+    for (int i = gl; i < n; i += G) z[i] = r[i];
+    __syncwarp();
+    ilu_g<G>(recl(l), act, z, gl);
+    residual_g<DIM, G>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, r, z, s, n, gl);
+    __syncwarp();
+    const double* Wx = P.W + P.woff[l][ec[0]];
+    const double* Wy = P.W + P.woff[l][ec[1]];
+    const double* Wz = P.W + P.woff[l][DIM == 3 ? ec[2] : 1];
+    const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
+    double* rc = rv(l + 1);
+    double* T2 = DIM == 3 ? T1 + cx * fy * fz : rc;
+    for (int t = gl; t < cx * fy * fz; t += G) {           // x pass
+      const int ic = t % cx, rest = t / cx;
+      double a = 0.0;
+      for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * s[f + fx * rest];
+      T1[t] = a;
+    }
+    __syncwarp();
+    for (int t = gl; t < cx * cy * fz; t += G) {           // y pass
+      const int ic = t % cx, jc = (t / cx) % cy, kf = t / (cx * cy);
+      double a = 0.0;
+      for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * T1[ic + cx * (f + fy * kf)];
+      T2[t] = a;
+    }
+    __syncwarp();
+    if (DIM == 3) {
+      for (int t = gl; t < cx * cy * cz; t += G) {         // z pass
+        const int ij = t % (cx * cy), kc = t / (cx * cy);
+        double a = 0.0;
+        for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * T2[ij + cx * cy * f];
+        rc[t] = a;
+      }
+      __syncwarp();
+    }
+  }
+  // ---- coarsest level: exact LDL^T (reading c8)
+  {
+    int lo[3], ext[3];
+    box(L - 1, lo, ext);
+    const int n = ext[0] * ext[1] * ext[2];
+    double *r = rv(L - 1), *z = zv(L - 1);
+    for (int i = gl; i < n; i += G) z[i] = r[i];
+    __syncwarp();
+    ilu_g<G>(recl(L - 1), act, z, gl);
+  }
+  // ---- upward leg: prolongate (separable P), residual, post-smooth
+  for (int l = L - 2; l >= 0; --l) {
+    int lo[3], ext[3], clo[3], cext[3];
+    box(l, lo, ext);
+    box(l + 1, clo, cext);
+    const int n = ext[0] * ext[1] * ext[2];
+    double *r = rv(l), *z = zv(l), *s = sv(l);
+    const double* e = zv(l + 1);
+    const double* Wx = P.W + P.woff[l][ec[0]];
+    const double* Wy = P.W + P.woff[l][ec[1]];
+    const double* Wz = P.W + P.woff[l][DIM == 3 ? ec[2] : 1];
+    const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
+    const double* U2 = e;
+    if (DIM == 3) {
+      double* U2w = T1 + cx * fy * fz;
+      for (int t = gl; t < cx * cy * fz; t += G) {         // z pass: [cx][cy][fz]
+        const int ij = t % (cx * cy), kf = t / (cx * cy);
+        double a = 0.0;
+        for (int c = 0; c < cz; ++c) a += __ldg(Wz + c * fz + kf) * e[ij + cx * cy * c];
+        U2w[t] = a;
+      }
+      __syncwarp();
+      U2 = U2w;
+    }
+    for (int t = gl; t < cx * fy * fz; t += G) {           // y pass: [cx][fy][fz]
+      const int ic = t % cx, jf = (t / cx) % fy, kf = t / (cx * fy);
+      double a = 0.0;
+      for (int c = 0; c < cy; ++c) a += __ldg(Wy + c * fy + jf) * U2[ic + cx * (c + cy * kf)];
+      T1[t] = a;
+    }
+    __syncwarp();
+    for (int i = gl; i < n; i += G) {                      // x pass, z += P e
+      const int fxi = i % fx, rest = i / fx;
+      double a = 0.0;
+      for (int c = 0; c < cx; ++c) a += __ldg(Wx + c * fx + fxi) * T1[c + cx * rest];
+      z[i] += a;
+    }
+    __syncwarp();
+    residual_g<DIM, G>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, r, z, s, n, gl);
+    __syncwarp();
+    ilu_g<G>(recl(l), act, s, gl);
+    for (int i = gl; i < n; i += G) z[i] += s[i];
+    __syncwarp();
+  }
+  // ---- z += I_j z_j (a8)
+  {
+    int lo[3], ext[3];
+    box(0, lo, ext);
+    const int n = ext[0] * ext[1] * ext[2];
+    const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+    const double* z0 = zv(0);
+    for (int i = gl; i < n; i += G) {
+      const int ix = i % ext[0], iy = (i / ext[0]) % ext[1], iz = i / (ext[0] * ext[1]);
+      atomicAdd(P.z + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)), z0[i]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ apply driver
+template <int DIM>
+static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  const lorpc_mesh* m = b->m;
+  int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, DIM == 3 ? m->n[2] + 1 : 1);
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
+  int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
+  k_restrict_vertex<DIM><<<nb(b->cN[0], 128), 128, 0, s>>>(r, b->cr[0], nv, N, m->basis);
+  LORPC_LAUNCHED();
+  const int K = b->nc - 1;
+  for (int l = 0; l < K; ++l) {
+    int3 Nv = i3(b->cn[l]), Nc = i3(b->cn[l + 1]);
+    k_jacobi_pre<DIM><<<nb(b->cN[l], 256), 256, 0, s>>>(b->cr[l], b->dl1[l], b->cz[l], Nv);
+    LORPC_LAUNCHED();
+    k_residual_grid<DIM><<<nb(b->cN[l], 256), 256, 0, s>>>(b->Ac[l], b->cr[l], b->cz[l], b->cs[l], Nv);
+    LORPC_LAUNCHED();
+    k_restrict_grid<DIM><<<nb(b->cN[l + 1], 256), 256, 0, s>>>(b->cs[l], b->cr[l + 1], Nv, Nc);
+    LORPC_LAUNCHED();
+  }
+  if (b->ncoarsest > 0) {
+    k_coarsest_solve<DIM><<<1, 1, 0, s>>>(b->coarse_chol, b->cr[K], b->cz[K], i3(b->cn[K]), b->ncoarsest);
+    LORPC_LAUNCHED();
+  } else {
+    LORPC_CUDA(cudaMemsetAsync(b->cz[K], 0, sizeof(double) * b->cN[K], s));
+  }
+  // level results: coarsest in cz[K], finer levels (after post-smoothing) in cs[l]
+  for (int l = K - 1; l >= 0; --l) {
+    int3 Nv = i3(b->cn[l]), Nc = i3(b->cn[l + 1]);
+    const double* ec = (l + 1 == K) ? b->cz[l + 1] : b->cs[l + 1];
+    k_prolong_grid_add<DIM><<<nb(b->cN[l], 256), 256, 0, s>>>(ec, b->cz[l], Nv, Nc);
+    LORPC_LAUNCHED();
+    k_jacobi_post<DIM><<<nb(b->cN[l], 256), 256, 0, s>>>(b->Ac[l], b->cr[l], b->dl1[l], b->cz[l], b->cs[l], Nv);
+    LORPC_LAUNCHED();
+  }
+  const double* z0 = (K == 0) ? b->cz[0] : b->cs[0];
+  k_prolong_vertex_add<DIM><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z0, z, nv, N, n, m->basis);
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+
+template <int DIM>
+__global__ void k_zero_dir(double* z, int3 N) {
+  const long long NT = (long long)N.x * N.y * N.z;
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  const int c0 = (int)(g % N.x), c1 = (int)((g / N.x) % N.y), c2 = (int)(g / ((long long)N.x * N.y));
+  bool dd = c0 == 0 || c0 == N.x - 1 || c1 == 0 || c1 == N.y - 1;
+  if (DIM == 3) dd = dd || c2 == 0 || c2 == N.z - 1;
+  if (dd) z[g] = 0.0;
+}
+
+template <int DIM, int G>
+static int launch_vcycle(const VcParams& P, long long J, cudaStream_t s) {
+  constexpr int PPW = 32 / G;
+  const size_t per_warp = (size_t)PPW * P.patch_doubles * sizeof(double);
+  int wpb = 4;
+  while (wpb > 1 && per_warp * wpb > 113 * 1024) wpb >>= 1;
+  const size_t smem = per_warp * wpb;
+  if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle: patch does not fit in shared memory");
+  const long long warps = (J + PPW - 1) / PPW;
+  const unsigned blocks = (unsigned)((warps + wpb - 1) / wpb);
+  cudaFuncSetAttribute(k_vcycle<DIM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_vcycle<DIM, G><<<blocks, 32 * wpb, smem, s>>>(P);
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+
+int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  const lorpc_mesh* m = b->m;
+  const lorpc_lor* lor = b->lor;
+  const int d = m->d, L = b->L;
+  LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * m->ndof_cg, s));
+  VcParams P{};
+  P.G = make_geom(b);
+  for (int l = 0; l < L; ++l) P.A[l] = lor->A[l];
+  P.W = b->wtab;
+  memcpy(P.woff, b->woff, sizeof(P.woff));
+  memcpy(P.wfe, b->wfe, sizeof(P.wfe));
+  memcpy(P.wce, b->wce, sizeof(P.wce));
+  P.rec = b->rec; P.recoff = b->recoff; P.J = b->J; P.r = r; P.z = z;
+  int acc = 0;
+  for (int l = 0; l < L; ++l) { P.soff[l] = acc; P.nmax[l] = b->max_n[l]; acc += 3 * b->max_n[l]; }
+  P.toff = acc;
+  acc += b->scratch_doubles;
+  acc = (acc + 1) & ~1;                 // 16-byte alignment of the staged record
+  P.roff = acc;
+  // Record staging in shared memory (one TMA bulk copy per patch) is an
+  // experiment switch: it caps residency at ~2 warps/SM (ncu r01, C5) and measured
+  // slower than reading the records through L1/L2.
+  static const bool stage = getenv("LORPC_STAGE") && getenv("LORPC_STAGE")[0] == '1';
+  P.rec_doubles = stage ? (int)(b->rec_max / 8) : 0;
+  acc += P.rec_doubles;
+  P.boff = acc;                         // mbarrier
+  acc += 2;
+  P.patch_doubles = acc;
+  P.rec_total = b->rec_bytes;
+  int G = b->lanes;
+  if (stage && !getenv("LORPC_LANES")) {
+    const size_t pp = (size_t)acc * 8;
+    G = pp * 8 <= 113 * 1024 ? 4 : pp * 4 <= 113 * 1024 ? 8 : pp * 2 <= 113 * 1024 ? 16 : 32;
+  }
+  lorpc_prec* bm = const_cast<lorpc_prec*>(b);
+  const bool prof = bm->prof_on && bm->prof_n < (int)bm->prof_ev.size() / 2;
+  if (prof) LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n], s));
+  int rc;
+  if (d == 2) {
+    rc = G == 4 ? launch_vcycle<2, 4>(P, b->J, s) : G == 8 ? launch_vcycle<2, 8>(P, b->J, s)
+       : G == 16 ? launch_vcycle<2, 16>(P, b->J, s) : launch_vcycle<2, 32>(P, b->J, s);
+  } else {
+    rc = G == 4 ? launch_vcycle<3, 4>(P, b->J, s) : G == 8 ? launch_vcycle<3, 8>(P, b->J, s)
+       : G == 16 ? launch_vcycle<3, 16>(P, b->J, s) : launch_vcycle<3, 32>(P, b->J, s);
+  }
+  if (rc != LORPC_OK) return rc;
+  if (prof) { LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n + 1], s)); bm->prof_n++; }
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
+  if (b->desc.coarse == 0) {
+    if (d == 2) LORPC_TRY(coarse_apply<2>(b, r, z, s)); else LORPC_TRY(coarse_apply<3>(b, r, z, s));
+  } else {
+    if (d == 2) k_zero_dir<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z, N);
+    else k_zero_dir<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z, N);
+    LORPC_LAUNCHED();
+  }
+  return LORPC_OK;
+}
+
+}  // namespace lorpc

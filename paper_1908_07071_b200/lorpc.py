@@ -43,7 +43,8 @@ class PcgReport(ctypes.Structure):
 SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc_quad_points",
            "lorpc_rhs_assemble", "lorpc_operator_apply", "lorpc_lor_assemble", "lorpc_lor_destroy",
            "lorpc_schwarz_setup", "lorpc_prec_destroy", "lorpc_precond_apply",
-           "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
+           "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_prec_bytes", "lorpc_prec_profile",
+           "lorpc_prec_profile_read", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
            "lorpc_launch_count", "lorpc_last_error"]
 
 
@@ -67,6 +68,9 @@ def lib():
         L.lorpc_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
         L.lorpc_prec_export_ordering.argtypes = [_vp, _ll, _int, ctypes.POINTER(_int), ctypes.POINTER(_int)]
         L.lorpc_prec_info.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_int)]
+        L.lorpc_prec_bytes.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
+        L.lorpc_prec_profile.argtypes = [_vp, _int]
+        L.lorpc_prec_profile_read.argtypes = [_vp, ctypes.POINTER(_d), ctypes.POINTER(_ll)]
         L.lorpc_pcg_solve.argtypes = [_vp, _vp, _vp, _vp, _d, _int, ctypes.POINTER(PcgReport), _vp]
         L.lorpc_pcg_solve_host.argtypes = [_vp, _vp, _vp, _vp, _d, _int, ctypes.POINTER(PcgReport), _vp]
         L.lorpc_launch_count.restype = _ll
@@ -170,6 +174,21 @@ class Prec:
 
     def apply(self, r, z, stream=None):
         _check(lib().lorpc_precond_apply(self.h, _dptr(r), _dptr(z), _stream(stream)))
+
+    def byte_model(self):
+        """(factor values, [level-l grid nodes], coarse GMG nodes) for the roofline model."""
+        fv, cn = _ll(), _ll()
+        ln = (_ll * 8)()
+        _check(lib().lorpc_prec_bytes(self.h, ctypes.byref(fv), ln, ctypes.byref(cn)))
+        return fv.value, [ln[i] for i in range(self.n_levels)], cn.value
+
+    def profile(self, enable):
+        _check(lib().lorpc_prec_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        ms, n = _d(), _ll()
+        _check(lib().lorpc_prec_profile_read(self.h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def ordering(self, patch, level, cap=1024):
         buf = (_int * cap)()
