@@ -178,8 +178,8 @@ class Problem:
         return cls(cfg.dim, cfg.n, cfg.p, vertices(cfg), disc=cfg.disc, eta=eta)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().or_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.or_destroy(self.h)
             self.h = None
 
     # --- operator -----------------------------------------------------------

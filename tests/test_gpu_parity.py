@@ -207,3 +207,78 @@ def test_full_size_operator_sampled_rows(L, name):
     yo = P.apply_rows(x, rows)
     yg = y.cpu().numpy()[rows]
     assert np.abs(yg - yo).max() <= TOL * max(np.abs(yo).max(), 1.0)
+
+
+# ---------------------------------------------------------------- SIPG DG (C4 recipe)
+DG_CASES = {
+    "C4s_c1": (small_config("C4", (3, 2, 3)), 1.0),
+    "C4s_c1000": (small_config("C4", (2, 3, 2)), 1000.0),
+    "C4p2_c10": (small_config("C4", (3, 3, 2), p=2), 10.0),
+    "C4pert_c10": (small_config("C2", (3, 2, 2), p=3), 10.0),
+}
+
+
+def _dg_cfg(name):
+    from dataclasses import replace
+    cfg, c = DG_CASES[name]
+    if cfg.dim != 3:  # perturbed 3D mesh with the C5 perturbation recipe
+        cfg = replace(small_config("C5", (3, 2, 2), p=3), disc="sipg", rhs="expsin")
+    return cfg, (cfg.p + 1) ** 2 * c
+
+
+def _dg_both(L, name):
+    cfg, eta = _dg_cfg(name)
+    V = vertices(cfg)
+    mesh = L.Mesh(3, cfg.n, cfg.p, V, disc=1, eta=eta)
+    P = O.Problem(3, cfg.n, cfg.p, V, disc="sipg", eta=eta)
+    return cfg, eta, mesh, P
+
+
+@pytest.mark.parametrize("name", list(DG_CASES))
+def test_dg_operator_parity(L, name):
+    cfg, eta, mesh, P = _dg_both(L, name)
+    x = parity_vector(P.ndof, seed=46)
+    y = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.apply(dev(x), y)
+    yo = P.apply(x)
+    assert rel(y.cpu().numpy(), yo) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C4s_c1", "C4pert_c10"])
+def test_dg_rhs_parity(L, name):
+    from workloads import dirichlet_function, rhs_function as rf
+    cfg, eta, mesh, P = _dg_both(L, name)
+    xq = torch.empty(mesh.n_quad * 3, dtype=torch.float64, device="cuda")
+    xb = torch.empty(mesh.n_bface_quad * 3, dtype=torch.float64, device="cuda")
+    mesh.quad_points(xq, xb)
+    Xo, Xbo = P.quad_points(), P.bface_points()
+    assert np.abs(xb.cpu().numpy().reshape(-1, 3) - Xbo).max() < 1e-14
+    fq = dev(rf(cfg, Xo))
+    gq = dev(dirichlet_function(cfg, Xbo))
+    b = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.rhs_assemble(fq, gq, b)
+    bo = P.rhs(rf(cfg, Xo))
+    P.rhs_bc(dirichlet_function(cfg, Xbo), bo)
+    assert rel(b.cpu().numpy(), bo) <= TOL
+
+
+@pytest.mark.parametrize("name", list(DG_CASES))
+def test_dg_precond_and_pcg_parity(L, name):
+    cfg, eta, mesh, P = _dg_both(L, name)
+    lor = L.Lor(mesh)
+    prec = L.Prec(lor)
+    P.schwarz_setup("vertex", "mdf", "gmg")
+    r = parity_vector(P.ndof, seed=47)
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    assert rel(z.cpu().numpy(), P.precond(r)) <= TOL
+    bo = P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty_like(z)
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, 1e-10)
+    xo, ro = P.pcg(bo, 1e-10)
+    # DG solves take ~100 iterations and the 2-norm residual oscillates near tol;
+    # rounding-level differences shift the crossing
+    assert abs(rep["iters"] - ro["iters"]) <= max(1, round(0.02 * ro["iters"]))
+    k = min(len(rep["res"]), len(ro["res"])) // 3
+    assert np.allclose(rep["res"][:k], ro["res"][:k], rtol=1e-3)
+    assert rel(x.cpu().numpy(), xo) <= 1e-8
