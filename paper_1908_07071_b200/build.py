@@ -9,7 +9,8 @@ OUT = os.path.join(HERE, "liblorpc.so")
 SOURCES = ["basis.cpp", "mesh.cu", "operator.cu", "lor.cu", "schwarz.cu", "vcycle.cu", "pcg.cu", "dg.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"] + \
+    os.environ.get("LORPC_NVCC_EXTRA", "").split()
 
 
 def build(force=False, verbose=False):

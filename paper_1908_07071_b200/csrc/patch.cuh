@@ -68,22 +68,52 @@ __host__ __device__ __forceinline__ long long a8(long long b) { return (b + 7) &
 //   bent[nL]  backward entries of row sched[t]: (k | pos << 16) with L[pos] = L_ki
 //   brow[n+1] row pointers into bent
 //   sched[n], lptr[n+1] (DAG level pointers), order[n] (elimination order)
-struct RecLayout { long long D, L, fnbr, frow, bent, brow, sched, lptr, order, total; };
+// Per patch-level ILU record (M = L D L^T).  The off-diagonal entries are stored
+// once, in forward-solve order: grouped by DAG level of the triangular solve,
+// within a level by row (schedule order), within a row by direction:
+//   D[n]        pivots (natural index)
+//   L[nL]       L_ij, row i = sched[lptr[lv] + seg], column j = nb
+//   nb[nL]      natural index j (u16)
+//   sg[nL]      row slot within its DAG level (u8)
+//   elev[n+1]   entry offset of each DAG level
+//   lptr[n+1]   row offset of each DAG level into sched
+//   sched[n]    rows in schedule order (natural index)
+//   order[n]    elimination order (export only)
+//   bk[nL], bp[nL], bsg[nL], belev[n+1]: the backward (L^T) entries, grouped the
+//     same way by DAG level and row i: upper neighbour k, position of L_ki in L,
+//     row slot of i within its level
+// Both sweeps pull, with a segmented warp reduction per row (deterministic).
+struct RecLayout { long long D, L, nb, sg, bk, bp, bsg, elev, belev, lptr, sched, order, total; };
 __host__ __device__ __forceinline__ RecLayout rec_layout(int n, long long nL) {
   RecLayout R;
   R.D = 16;
   R.L = R.D + 8ll * n;
-  R.fnbr = R.L + 8ll * nL;
-  R.frow = R.fnbr + a8(2ll * nL);
-  R.bent = R.frow + a8(2ll * (n + 1));
-  R.brow = R.bent + a8(4ll * nL);
-  R.sched = R.brow + a8(2ll * (n + 1));
-  R.lptr = R.sched + a8(2ll * n);
-  R.order = R.lptr + a8(2ll * (n + 1));
+  R.nb = R.L + 8ll * nL;
+  R.sg = R.nb + a8(2ll * nL);
+  R.bk = R.sg + a8(nL);
+  R.bp = R.bk + a8(2ll * nL);
+  R.bsg = R.bp + a8(2ll * nL);
+  R.elev = R.bsg + a8(nL);
+  R.belev = R.elev + a8(2ll * (n + 1));
+  R.lptr = R.belev + a8(2ll * (n + 1));
+  R.sched = R.lptr + a8(2ll * (n + 1));
+  R.order = R.sched + a8(2ll * n);
   R.total = (R.order + 2ll * n + 15) & ~15ll;  // 16-byte aligned patch records
   return R;
 }
 
+
+// floor(i / d) for 0 <= i < 2^20 and small d, from a precomputed float 1/d
+// (margin 0.5/d against the float rounding of (i + 0.5)/d): avoids the ~20-
+// instruction integer division in the per-node index arithmetic.
+__device__ __forceinline__ int qdiv(int i, float rd) { return __float2int_rz(((float)i + 0.5f) * rd); }
+// (x, y, z) of a box index i in an ex x ey x ez box
+__device__ __forceinline__ void box_xyz(int i, int ex, int ey, float rex, float rexy, int& x, int& y, int& z) {
+  z = qdiv(i, rexy);
+  const int r = i - z * ex * ey;
+  y = qdiv(r, rex);
+  x = r - y * ex;
+}
 
 template <int DIM>
 __device__ __forceinline__ int doff(int d, int ex, int ey) {

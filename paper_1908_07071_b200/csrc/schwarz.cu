@@ -194,15 +194,14 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       __syncwarp();
     }
     if (failed) continue;
-    // ---- record (layout: rec_layout)
+    // ---- record (layout: rec_layout in patch.cuh)
     double* Dr = (double*)(rec + R.D);
     double* Lr = (double*)(rec + R.L);
-    uint16_t* fnbr = (uint16_t*)(rec + R.fnbr);
-    uint16_t* frow = (uint16_t*)(rec + R.frow);
-    uint32_t* bent = (uint32_t*)(rec + R.bent);
-    uint16_t* brow = (uint16_t*)(rec + R.brow);
-    uint16_t* sch = (uint16_t*)(rec + R.sched);
+    uint16_t* nbr = (uint16_t*)(rec + R.nb);
+    uint8_t* sgr = (uint8_t*)(rec + R.sg);
+    uint16_t* elv = (uint16_t*)(rec + R.elev);
     uint16_t* lpt = (uint16_t*)(rec + R.lptr);
+    uint16_t* sch = (uint16_t*)(rec + R.sched);
     uint16_t* orr = (uint16_t*)(rec + R.order);
     for (int i = lane; i < n; i += 32) {
       Dr[i] = At[i * ND + C];  // pivot at elimination time (never modified afterwards)
@@ -239,37 +238,49 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       for (int v = 0; v < depth; ++v) { lpt[v] = (uint16_t)acc; const int c = cnt[v]; cnt[v] = acc; acc += c; }
       lpt[depth] = (uint16_t)acc;
       for (int t = 0; t < n; ++t) { const int i = ord[t]; sch[cnt[lev[i]]++] = (uint16_t)i; }
-      // forward rows (lower entries) in schedule order
+      // entries grouped by level, then row, then direction
       int e = 0;
-      for (int t = 0; t < n; ++t) {
-        const int i = sch[t];
-        frow[t] = (uint16_t)e;
-        uint32_t lm = (uint32_t)lmk[i];
-        while (lm) {
-          const int d = __ffs(lm) - 1;
-          lm &= lm - 1;
-          Lr[e] = Lf[i * ND + d];
-          fnbr[e] = (uint16_t)(i + doff<DIM>(d, ex, ey));
-          pmap[i * ND + d] = e;
-          ++e;
+      for (int v = 0; v < depth; ++v) {
+        elv[v] = (uint16_t)e;
+        for (int t = lpt[v]; t < lpt[v + 1]; ++t) {
+          const int i = sch[t];
+          uint32_t lm = (uint32_t)lmk[i];
+          while (lm) {
+            const int d = __ffs(lm) - 1;
+            lm &= lm - 1;
+            Lr[e] = Lf[i * ND + d];
+            nbr[e] = (uint16_t)(i + doff<DIM>(d, ex, ey));
+            sgr[e] = (uint8_t)(t - lpt[v]);
+            pmap[i * ND + d] = e;
+            ++e;
+          }
         }
       }
-      frow[n] = (uint16_t)e;
-      // backward rows (upper entries L_ki of later neighbours k) in schedule order
+      elv[depth] = (uint16_t)e;
+      // backward entries: row i pulls L_ki z_k from its later neighbours k
+      uint16_t* bk = (uint16_t*)(rec + R.bk);
+      uint16_t* bp = (uint16_t*)(rec + R.bp);
+      uint8_t* bsg = (uint8_t*)(rec + R.bsg);
+      uint16_t* belv = (uint16_t*)(rec + R.belev);
       int f = 0;
-      for (int t = 0; t < n; ++t) {
-        const int i = sch[t];
-        brow[t] = (uint16_t)f;
-        const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
-        uint32_t um = exist_mask<DIM>(ix, iy, iz, ex, ey, ez) & ~(uint32_t)lmk[i] & ~(1u << C);
-        while (um) {
-          const int d = __ffs(um) - 1;
-          um &= um - 1;
-          const int k = i + doff<DIM>(d, ex, ey);
-          bent[f++] = (uint32_t)k | ((uint32_t)pmap[k * ND + (ND - 1 - d)] << 16);
+      for (int v = 0; v < depth; ++v) {
+        belv[v] = (uint16_t)f;
+        for (int t = lpt[v]; t < lpt[v + 1]; ++t) {
+          const int i = sch[t];
+          const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
+          uint32_t um = exist_mask<DIM>(ix, iy, iz, ex, ey, ez) & ~(uint32_t)lmk[i] & ~(1u << C);
+          while (um) {
+            const int d = __ffs(um) - 1;
+            um &= um - 1;
+            const int k = i + doff<DIM>(d, ex, ey);
+            bk[f] = (uint16_t)k;
+            bp[f] = (uint16_t)pmap[k * ND + (ND - 1 - d)];
+            bsg[f] = (uint8_t)(t - lpt[v]);
+            ++f;
+          }
         }
       }
-      brow[n] = (uint16_t)f;
+      belv[depth] = (uint16_t)f;
       int* h = (int*)rec;
       h[0] = n; h[1] = depth; h[2] = (int)nL; h[3] = l;
     }
@@ -452,7 +463,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
     for (int l = 0; l < L; ++l) per_patch += 3 * b->max_n[l];
     (void)per_patch;
     // measured best among {4, 8, 16, 32} lanes (r01 probe): C5 (125-node patches) 16, C3 (343) 32
-    b->lanes = b->max_n[0] >= 300 ? 32 : 16;
+    b->lanes = 32;  // with 64-register V-cycle kernels (r01 probe: C5 161 ms vs 202 ms at G=16)
     if (const char* e = getenv("LORPC_LANES")) b->lanes = atoi(e);
   }
   // coarse space hierarchy (reading c11): level 0 = last LOR level (vertex grid)

@@ -5,6 +5,10 @@
 
 #include "patch.cuh"
 
+#ifndef LORPC_VC_MINB
+#define LORPC_VC_MINB 8   // min resident 128-thread blocks per SM for the V-cycle kernel
+#endif
+
 namespace lorpc {
 
 // ------------------------------------------------------------------ coarse space R_0
@@ -198,7 +202,33 @@ struct VcParams {
   double* z;
 };
 
-// v := M^{-1} v, M = L D L^T of one patch level (group-local lanes gl in [0,G))
+// One DAG level of a triangular sweep by the G lanes of a group: the level's
+// entries [eb, ee) are contiguous; each lane multiplies one entry, a segmented
+// shuffle reduction sums each row's entries (rows are contiguous, slots
+// non-decreasing), and the row's first lane subtracts the sum.  Rows of one level
+// are independent, so chunks need no synchronisation between them.
+template <int G>
+__device__ __forceinline__ void seg_level(const double* L, const uint16_t* col, const uint16_t* pos,
+                                          const uint8_t* sg, const uint16_t* sch, int eb, int ee, int rb,
+                                          double* v, int gl, unsigned gmask) {
+  for (int c0 = eb; c0 < ee; c0 += G) {
+    const int q = c0 + gl;
+    const bool in = q < ee;
+    double val = 0.0;
+    int seg = 1024 + gl;
+    if (in) { val = L[pos ? pos[q] : q] * v[col[q]]; seg = sg[q]; }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+      const double ov = __shfl_down_sync(gmask, val, off, G);
+      const int os = __shfl_down_sync(gmask, seg, off, G);
+      if (gl + off < G && os == seg) val += ov;
+    }
+    const int ps = __shfl_up_sync(gmask, seg, 1, G);
+    if (in && (gl == 0 || ps != seg)) v[sch[rb + seg]] -= val;
+  }
+}
+
+// v := M^{-1} v, M = L D L^T of one patch level (forward L, diagonal, backward L^T)
 template <int G>
 __device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int gl) {
   int n = 0, depth = 0, nL = 0;
@@ -208,53 +238,24 @@ __device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int 
   const RecLayout R = rec_layout(n, nL);
   const double* D = (const double*)(rec + R.D);
   const double* L = (const double*)(rec + R.L);
-  const uint16_t* fnbr = (const uint16_t*)(rec + R.fnbr);
-  const uint16_t* frow = (const uint16_t*)(rec + R.frow);
-  const uint32_t* bent = (const uint32_t*)(rec + R.bent);
-  const uint16_t* brow = (const uint16_t*)(rec + R.brow);
-  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* nb = (const uint16_t*)(rec + R.nb);
+  const uint8_t* sg = (const uint8_t*)(rec + R.sg);
+  const uint16_t* bk = (const uint16_t*)(rec + R.bk);
+  const uint16_t* bp = (const uint16_t*)(rec + R.bp);
+  const uint8_t* bsg = (const uint8_t*)(rec + R.bsg);
+  const uint16_t* elv = (const uint16_t*)(rec + R.elev);
+  const uint16_t* belv = (const uint16_t*)(rec + R.belev);
   const uint16_t* lpt = (const uint16_t*)(rec + R.lptr);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (((threadIdx.x & 31) / G) * G));
   for (int lv = 0; lv < md; ++lv) {
-    if (lv < depth) {
-      const int b = lpt[lv], e = lpt[lv + 1];
-      for (int t = b + gl; t < e; t += G) {
-        const int i = sch[t];
-        const int e0 = frow[t], e1 = frow[t + 1];
-        double a0 = v[i], a1 = 0.0;
-        int q = e0;
-        // batches of 4 independent (index, value, v) loads before the FMAs
-        for (; q + 4 <= e1; q += 4) {
-          const int n0 = fnbr[q], n1 = fnbr[q + 1], n2 = fnbr[q + 2], n3 = fnbr[q + 3];
-          const double l0 = L[q], l1 = L[q + 1], l2 = L[q + 2], l3 = L[q + 3];
-          const double v0 = v[n0], v1 = v[n1], v2 = v[n2], v3 = v[n3];
-          a0 -= l0 * v0; a1 += l1 * v1; a0 -= l2 * v2; a1 += l3 * v3;
-        }
-        for (; q < e1; ++q) a0 -= L[q] * v[fnbr[q]];
-        v[i] = a0 - a1;
-      }
-    }
+    if (lv < depth) seg_level<G>(L, nb, nullptr, sg, sch, elv[lv], elv[lv + 1], lpt[lv], v, gl, gmask);
     __syncwarp();
   }
   for (int i = gl; i < n; i += G) v[i] = v[i] / D[i];
   __syncwarp();
   for (int lv = md - 1; lv >= 0; --lv) {
-    if (lv < depth) {
-      const int b = lpt[lv], e = lpt[lv + 1];
-      for (int t = b + gl; t < e; t += G) {
-        const int i = sch[t];
-        const int e0 = brow[t], e1 = brow[t + 1];
-        double a0 = v[i], a1 = 0.0;
-        int q = e0;
-        for (; q + 4 <= e1; q += 4) {
-          const uint32_t u0 = bent[q], u1 = bent[q + 1], u2 = bent[q + 2], u3 = bent[q + 3];
-          const double l0 = L[u0 >> 16], l1 = L[u1 >> 16], l2 = L[u2 >> 16], l3 = L[u3 >> 16];
-          const double v0 = v[u0 & 0xffffu], v1 = v[u1 & 0xffffu], v2 = v[u2 & 0xffffu], v3 = v[u3 & 0xffffu];
-          a0 -= l0 * v0; a1 += l1 * v1; a0 -= l2 * v2; a1 += l3 * v3;
-        }
-        for (; q < e1; ++q) { const uint32_t u0 = bent[q]; a0 -= L[u0 >> 16] * v[u0 & 0xffffu]; }
-        v[i] = a0 - a1;
-      }
-    }
+    if (lv < depth) seg_level<G>(L, bk, bp, bsg, sch, belv[lv], belv[lv + 1], lpt[lv], v, gl, gmask);
     __syncwarp();
   }
 }
@@ -265,8 +266,10 @@ __device__ __forceinline__ void residual_g(const double* __restrict__ A, long lo
                                            const int* ext, const double* r, const double* z, double* s, int n, int gl) {
   constexpr int ND = Dirs<DIM>::ND;
   const int ex = ext[0], ey = ext[1], ez = ext[2];
+  const float rex = 1.0f / ex, rexy = 1.0f / (ex * ey);
   for (int i = gl; i < n; i += G) {
-    const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
+    int ix, iy, iz;
+    box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
     const long long gi = (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0));
     const double* Ar = A + gi * ND;
     const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
@@ -282,7 +285,7 @@ __device__ __forceinline__ void residual_g(const double* __restrict__ A, long lo
 }
 
 template <int DIM, int G>
-__global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
+__global__ void __launch_bounds__(128, LORPC_VC_MINB) k_vcycle(VcParams P) {
   constexpr int PPW = 32 / G;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
@@ -350,8 +353,10 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
     const int n = ext[0] * ext[1] * ext[2];
     const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
     double* r0 = rv(0);
+    const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
     for (int i = gl; i < n; i += G) {
-      const int ix = i % ext[0], iy = (i / ext[0]) % ext[1], iz = i / (ext[0] * ext[1]);
+      int ix, iy, iz;
+      box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
       r0[i] = __ldg(P.r + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)));
     }
   }
@@ -374,15 +379,16 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
     const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
     double* rc = rv(l + 1);
     double* T2 = DIM == 3 ? T1 + cx * fy * fz : rc;
+    const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
     for (int t = gl; t < cx * fy * fz; t += G) {           // x pass
-      const int ic = t % cx, rest = t / cx;
+      const int rest = qdiv(t, rcx), ic = t - rest * cx;
       double a = 0.0;
       for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * s[f + fx * rest];
       T1[t] = a;
     }
     __syncwarp();
     for (int t = gl; t < cx * cy * fz; t += G) {           // y pass
-      const int ic = t % cx, jc = (t / cx) % cy, kf = t / (cx * cy);
+      const int kf = qdiv(t, rcxy), r2 = t - kf * cx * cy, jc = qdiv(r2, rcx), ic = r2 - jc * cx;
       double a = 0.0;
       for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * T1[ic + cx * (f + fy * kf)];
       T2[t] = a;
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
     __syncwarp();
     if (DIM == 3) {
       for (int t = gl; t < cx * cy * cz; t += G) {         // z pass
-        const int ij = t % (cx * cy), kc = t / (cx * cy);
+        const int kc = qdiv(t, rcxy), ij = t - kc * cx * cy;
         double a = 0.0;
         for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * T2[ij + cx * cy * f];
         rc[t] = a;
@@ -421,10 +427,11 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
     const double* Wz = P.W + P.woff[l][DIM == 3 ? ec[2] : 1];
     const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
     const double* U2 = e;
+    const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
     if (DIM == 3) {
       double* U2w = T1 + cx * fy * fz;
       for (int t = gl; t < cx * cy * fz; t += G) {         // z pass: [cx][cy][fz]
-        const int ij = t % (cx * cy), kf = t / (cx * cy);
+        const int kf = qdiv(t, rcxy), ij = t - kf * cx * cy;
         double a = 0.0;
         for (int c = 0; c < cz; ++c) a += __ldg(Wz + c * fz + kf) * e[ij + cx * cy * c];
         U2w[t] = a;
@@ -433,14 +440,14 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
       U2 = U2w;
     }
     for (int t = gl; t < cx * fy * fz; t += G) {           // y pass: [cx][fy][fz]
-      const int ic = t % cx, jf = (t / cx) % fy, kf = t / (cx * fy);
+      const int kf = qdiv(t, rcxfy), r2 = t - kf * cx * fy, jf = qdiv(r2, rcx), ic = r2 - jf * cx;
       double a = 0.0;
       for (int c = 0; c < cy; ++c) a += __ldg(Wy + c * fy + jf) * U2[ic + cx * (c + cy * kf)];
       T1[t] = a;
     }
     __syncwarp();
     for (int i = gl; i < n; i += G) {                      // x pass, z += P e
-      const int fxi = i % fx, rest = i / fx;
+      const int rest = qdiv(i, rfx), fxi = i - rest * fx;
       double a = 0.0;
       for (int c = 0; c < cx; ++c) a += __ldg(Wx + c * fx + fxi) * T1[c + cx * rest];
       z[i] += a;
@@ -459,8 +466,10 @@ __global__ void __launch_bounds__(128, 4) k_vcycle(VcParams P) {
     const int n = ext[0] * ext[1] * ext[2];
     const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
     const double* z0 = zv(0);
+    const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
     for (int i = gl; i < n; i += G) {
-      const int ix = i % ext[0], iy = (i / ext[0]) % ext[1], iz = i / (ext[0] * ext[1]);
+      int ix, iy, iz;
+      box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
       atomicAdd(P.z + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)), z0[i]);
     }
   }
@@ -552,9 +561,8 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   acc += b->scratch_doubles;
   acc = (acc + 1) & ~1;                 // 16-byte alignment of the staged record
   P.roff = acc;
-  // Record staging in shared memory (one TMA bulk copy per patch) is an
-  // experiment switch: it caps residency at ~2 warps/SM (ncu r01, C5) and measured
-  // slower than reading the records through L1/L2.
+  // Patch records are read through L1/L2 (LORPC_STAGE=1 stages each patch's records
+  // in shared memory with one TMA bulk copy; measured slower: SMEM caps the warps).
   static const bool stage = getenv("LORPC_STAGE") && getenv("LORPC_STAGE")[0] == '1';
   P.rec_doubles = stage ? (int)(b->rec_max / 8) : 0;
   acc += P.rec_doubles;
@@ -563,10 +571,6 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   P.patch_doubles = acc;
   P.rec_total = b->rec_bytes;
   int G = b->lanes;
-  if (stage && !getenv("LORPC_LANES")) {
-    const size_t pp = (size_t)acc * 8;
-    G = pp * 8 <= 113 * 1024 ? 4 : pp * 4 <= 113 * 1024 ? 8 : pp * 2 <= 113 * 1024 ? 16 : 32;
-  }
   lorpc_prec* bm = const_cast<lorpc_prec*>(b);
   const bool prof = bm->prof_on && bm->prof_n < (int)bm->prof_ev.size() / 2;
   if (prof) LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n], s));
