@@ -216,7 +216,7 @@ __device__ __forceinline__ void seg_level(const double* L, const uint16_t* col, 
     const bool in = q < ee;
     double val = 0.0;
     int seg = 1024 + gl;
-    if (in) { val = L[pos ? pos[q] : q] * v[col[q]]; seg = sg[q]; }
+    if (in) { val = __ldg(L + (pos ? __ldg(pos + q) : q)) * v[__ldg(col + q)]; seg = __ldg(sg + q); }
 #pragma unroll
     for (int off = 1; off < G; off <<= 1) {
       const double ov = __shfl_down_sync(gmask, val, off, G);
@@ -224,7 +224,7 @@ __device__ __forceinline__ void seg_level(const double* L, const uint16_t* col, 
       if (gl + off < G && os == seg) val += ov;
     }
     const int ps = __shfl_up_sync(gmask, seg, 1, G);
-    if (in && (gl == 0 || ps != seg)) v[sch[rb + seg]] -= val;
+    if (in && (gl == 0 || ps != seg)) v[__ldg(sch + rb + seg)] -= val;
   }
 }
 
@@ -232,7 +232,7 @@ __device__ __forceinline__ void seg_level(const double* L, const uint16_t* col, 
 template <int G>
 __device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int gl) {
   int n = 0, depth = 0, nL = 0;
-  if (act) { const int* h = (const int*)rec; n = h[0]; depth = h[1]; nL = h[2]; }
+  if (act) { const int4 h = __ldg((const int4*)rec); n = h.x; depth = h.y; nL = h.z; }
   const int md = __reduce_max_sync(0xffffffffu, depth);
   if (md == 0) return;
   const RecLayout R = rec_layout(n, nL);
@@ -249,13 +249,15 @@ __device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int 
   const uint16_t* sch = (const uint16_t*)(rec + R.sched);
   const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (((threadIdx.x & 31) / G) * G));
   for (int lv = 0; lv < md; ++lv) {
-    if (lv < depth) seg_level<G>(L, nb, nullptr, sg, sch, elv[lv], elv[lv + 1], lpt[lv], v, gl, gmask);
+    if (lv < depth)
+      seg_level<G>(L, nb, nullptr, sg, sch, __ldg(elv + lv), __ldg(elv + lv + 1), __ldg(lpt + lv), v, gl, gmask);
     __syncwarp();
   }
-  for (int i = gl; i < n; i += G) v[i] = v[i] / D[i];
+  for (int i = gl; i < n; i += G) v[i] = v[i] / __ldg(D + i);
   __syncwarp();
   for (int lv = md - 1; lv >= 0; --lv) {
-    if (lv < depth) seg_level<G>(L, bk, bp, bsg, sch, belv[lv], belv[lv + 1], lpt[lv], v, gl, gmask);
+    if (lv < depth)
+      seg_level<G>(L, bk, bp, bsg, sch, __ldg(belv + lv), __ldg(belv + lv + 1), __ldg(lpt + lv), v, gl, gmask);
     __syncwarp();
   }
 }
@@ -563,7 +565,7 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   P.roff = acc;
   // Patch records are read through L1/L2 (LORPC_STAGE=1 stages each patch's records
   // in shared memory with one TMA bulk copy; measured slower: SMEM caps the warps).
-  static const bool stage = getenv("LORPC_STAGE") && getenv("LORPC_STAGE")[0] == '1';
+  const bool stage = false;  // records are read with __ldg: the staged variant is retired
   P.rec_doubles = stage ? (int)(b->rec_max / 8) : 0;
   acc += P.rec_doubles;
   P.boff = acc;                         // mbarrier
