@@ -55,8 +55,11 @@ typedef struct {
   int dim;      /* 2 or 3 */
   int n[3];     /* elements per axis (n[2] ignored in 2D) */
   int p;        /* polynomial degree; compiled set: 2D p in {2..8}, 3D p in {2..6} */
-  int disc;     /* 0 = continuous H1 (CG), 1 = symmetric interior penalty DG */
-  double eta;   /* SIPG only: sigma_e = eta / h_e, h_e = min(|K-|,|K+|)/|e| (readings c13, c14) */
+  int disc;     /* 0 = continuous H1 (CG), 1 = symmetric interior penalty DG (eq:ip),
+                   2 = BR2 DG (eq:br2 P:152-158, lifting eq:lift P:662-665; affine elements only,
+                   LORPC_ERR_SIZE otherwise).  DG requires dim = 3. */
+  double eta;   /* SIPG: sigma_e = eta / h_e, h_e = min(|K-|,|K+|)/|e| (readings c13, c14);
+                   BR2: coefficient of sum_e (r_e([u]), r_e([v])) */
 } lorpc_mesh_desc;
 
 /* Additive Schwarz B = sum_{j=0}^J R_j Q_j (eq:as P:274-277). */

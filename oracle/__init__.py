@@ -168,7 +168,7 @@ class Problem:
         self.nloc = (p + 1) ** dim
         self.n_el = int(np.prod(self.n))
         if disc != "cg":
-            _check(lib().or_set_dg(self.h, 1, float(eta)))
+            _check(lib().or_set_dg(self.h, {"sipg": 1, "br2": 2}[disc], float(eta)))
         self.ndof_cg = lib().or_ndof(self.h)
         self.ndof = self.ndof_cg if disc == "cg" else self.n_el * self.nloc
 

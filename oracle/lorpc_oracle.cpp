@@ -484,6 +484,7 @@ struct Problem {
   vec C0dense; int n0dense = 0;         // coarse=2: exact A_0 solve
   // DG
   vec DB;                               // diag(A_IP) (full DG vector)
+  std::vector<vec> br2C;                // BR2: Cholesky factors of the element mass matrices
 };
 
 extern "C" void* or_create(int d, int n0, int n1, int n2, int p, const double* vertices) {

@@ -1,4 +1,5 @@
 // C ABI (include/lorpc.h): argument checking, handle lifetime, dispatch.
+#include <cmath>
 #include <cstring>
 
 #include "device.cuh"
@@ -38,8 +39,31 @@ int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, 
   if (desc->p < 1) return fail(LORPC_ERR_ARG, "mesh_create: p must be >= 1");
   if ((d == 2 && desc->p > 8) || (d == 3 && desc->p > 6)) return fail(LORPC_ERR_SIZE, "mesh_create: p not compiled");
   for (int k = 0; k < d; ++k) if (desc->n[k] < 1) return fail(LORPC_ERR_ARG, "mesh_create: n must be >= 1");
-  if (desc->disc != 0 && desc->disc != 1) return fail(LORPC_ERR_ARG, "mesh_create: disc must be 0 (CG) or 1 (SIPG)");
-  if (desc->disc == 1 && !(desc->eta > 0.0)) return fail(LORPC_ERR_ARG, "mesh_create: eta must be > 0");
+  if (desc->disc < 0 || desc->disc > 2) return fail(LORPC_ERR_ARG, "mesh_create: disc must be 0 (CG), 1 (SIPG), 2 (BR2)");
+  if (desc->disc != 0 && !(desc->eta > 0.0)) return fail(LORPC_ERR_ARG, "mesh_create: eta must be > 0");
+  if (desc->disc != 0 && d != 3) return fail(LORPC_ERR_SIZE, "mesh_create: DG is built for 3D meshes");
+  if (desc->disc == 2) {
+    // the BR2 lifting kernels use M_K = det J (M1 x M1 x M1): elements must be affine
+    // (parallelepipeds): the mixed terms of every trilinear map must vanish
+    const int nx = desc->n[0], ny = desc->n[1], nz = desc->n[2];
+    auto V = [&](int i, int j, int k, int c) {
+      return vertices_host[(((long long)k * (ny + 1) + j) * (nx + 1) + i) * 3 + c];
+    };
+    for (int k = 0; k < nz; ++k)
+      for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i)
+          for (int c = 0; c < 3; ++c) {
+            const double ex = V(i + 1, j, k, c) - V(i, j, k, c);
+            const double sc = std::fabs(ex) + std::fabs(V(i, j + 1, k, c) - V(i, j, k, c)) +
+                              std::fabs(V(i, j, k + 1, c) - V(i, j, k, c)) + 1e-300;
+            const double mxy = V(i + 1, j + 1, k, c) - V(i + 1, j, k, c) - V(i, j + 1, k, c) + V(i, j, k, c);
+            const double mxz = V(i + 1, j, k + 1, c) - V(i + 1, j, k, c) - V(i, j, k + 1, c) + V(i, j, k, c);
+            const double myz = V(i, j + 1, k + 1, c) - V(i, j + 1, k, c) - V(i, j, k + 1, c) + V(i, j, k, c);
+            if (std::fabs(mxy) + std::fabs(mxz) + std::fabs(myz) > 1e-12 * sc)
+              return fail(LORPC_ERR_SIZE, "mesh_create: BR2 needs affine (parallelepiped) elements; element " +
+                                              std::to_string(i + (long long)nx * (j + (long long)ny * k)) + " is not");
+          }
+  }
   lorpc_mesh* m = new lorpc_mesh();
   m->desc = *desc;
   m->d = d; m->p = desc->p; m->q = desc->p + 1;

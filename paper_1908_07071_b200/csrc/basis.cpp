@@ -88,6 +88,30 @@ void make_basis(int p, Basis1D& B) {
   }
   eval(0.0L, v, d); for (int j = 0; j <= p; ++j) B.E0[j] = (double)d[j];
   eval(1.0L, v, d); for (int j = 0; j <= p; ++j) B.E1[j] = (double)d[j];
+  // inverse of the reference 1D mass matrix M1 = B^T diag(w) B (Gauss-Jordan, long double)
+  const int m = p + 1;
+  long double A[MAXP + 1][2 * (MAXP + 1)];
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      long double s = 0.0L;
+      for (int k = 0; k < q; ++k) s += (long double)B.wq[k] * B.B[k * m + i] * B.B[k * m + j];
+      A[i][j] = s;
+      A[i][m + j] = (i == j) ? 1.0L : 0.0L;
+    }
+  for (int c = 0; c < m; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < m; ++r) if (std::fabs((double)A[r][c]) > std::fabs((double)A[piv][c])) piv = r;
+    for (int j = 0; j < 2 * m; ++j) std::swap(A[c][j], A[piv][j]);
+    const long double inv = 1.0L / A[c][c];
+    for (int j = 0; j < 2 * m; ++j) A[c][j] *= inv;
+    for (int r = 0; r < m; ++r) {
+      if (r == c) continue;
+      const long double f = A[r][c];
+      for (int j = 0; j < 2 * m; ++j) A[r][j] -= f * A[c][j];
+    }
+  }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) B.M1inv[i * m + j] = (double)A[i][m + j];
 }
 
 std::vector<std::vector<int>> make_chain(int p) {

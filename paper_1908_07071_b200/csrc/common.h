@@ -56,6 +56,7 @@ struct Basis1D {
   double B[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j(x_q)
   double D[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j'(x_q)
   double E0[MAXP + 1], E1[MAXP + 1];  // l_j'(0), l_j'(1) (face normal derivatives)
+  double M1inv[(MAXP + 1) * (MAXP + 1)];  // inverse of the reference 1D mass B^T W B (BR2 lifting)
 };
 void make_basis(int p, Basis1D& b);                 // basis.cpp
 std::vector<std::vector<int>> make_chain(int p);    // basis.cpp (reading c3)

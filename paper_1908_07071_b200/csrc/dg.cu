@@ -181,7 +181,7 @@ template <int P>
 __global__ void __launch_bounds__((P + 1) * (P + 1))
 k_dgface3(int mode, int axis, int bside, const double* __restrict__ x, double* __restrict__ y,
           const double* __restrict__ gq, const double* __restrict__ V, const double* __restrict__ vol, int3 n,
-          Basis1D bs, double eta) {
+          Basis1D bs, double eta, int br2) {
   constexpr int Q = P + 1, Q2 = Q * Q, NL = Q * Q * Q;
   __shared__ double su[2][NL];
   __shared__ double T0[2][Q2], T1[2][Q2];
@@ -287,6 +287,59 @@ k_dgface3(int mode, int axis, int bside, const double* __restrict__ x, double* _
   if (hm && hp) hv = fmin(vol[em], vol[ep]);
   else hv = vol[hm ? em : ep];
   const double sigma = eta / (hv / area);
+  // the jump J at this point ([u] = J n): interior u^- - u^+, boundary u (or the data g)
+  double Jq = 0.0;
+  if (mode == 0) Jq = (hm && hp) ? u[0] - u[1] : u[sref];
+  else Jq = gq[(long long)blockIdx.x * Q2 + tid];
+  // BR2 (eq:br2, lifting eq:lift): the penalty value sigma J is replaced by
+  //   g = eta sum_K s_K^2 sum_m n_m W_m^K,  W_m^K = sum_i (M_K^{-1} b_m^K)_i psi_i^K,
+  //   b_m^K,i = int_e J n_m psi_i^K.
+  // Affine elements: M_K = det J_K (M1 x M1 x M1), only face nodes of K see the face,
+  // so M_K^{-1} on them is (M1^{-1})_{end,end} (M1^{-1} x M1^{-1}) / det J_K and the two
+  // sides share b (same tangential basis); flat faces: sum_m n_m n_m = 1.
+  double pen = sigma * Jq;
+  if (br2) {
+    X0[0][tid] = dS * Jq;
+    __syncthreads();
+    {  // beta[i][j] = sum_q B[q1][i] B[q2][j] dS J   (transpose interpolation)
+      double a = 0.0;
+      for (int q1 = 0; q1 < Q; ++q1) a += bs.B[q1 * Q + qi] * X0[0][q1 + Q * qj];
+      X1[0][qi + Q * qj] = a;
+    }
+    __syncthreads();
+    {
+      double a = 0.0;
+      for (int q2 = 0; q2 < Q; ++q2) a += bs.B[q2 * Q + qj] * X1[0][qi + Q * q2];
+      X2[0][tid] = a;  // beta[qi][qj]
+    }
+    __syncthreads();
+    {  // c = (M1^{-1} x M1^{-1}) beta
+      double a = 0.0;
+      for (int i2 = 0; i2 < Q; ++i2) a += bs.M1inv[qi * Q + i2] * X2[0][i2 + Q * qj];
+      X0[1][tid] = a;
+    }
+    __syncthreads();
+    {
+      double a = 0.0;
+      for (int j2 = 0; j2 < Q; ++j2) a += bs.M1inv[qj * Q + j2] * X0[1][qi + Q * j2];
+      X1[1][tid] = a;  // c[qi][qj]
+    }
+    __syncthreads();
+    {  // W at the point (q1 = qi, q2 = qj)
+      double a = 0.0;
+      for (int i = 0; i < Q; ++i) a += bs.B[qi * Q + i] * X1[1][i + Q * qj];
+      X2[1][qi + Q * qj] = a;
+    }
+    __syncthreads();
+    double W = 0.0;
+    for (int j = 0; j < Q; ++j) W += bs.B[qj * Q + j] * X2[1][qi + Q * j];
+    const double kap = bs.M1inv[0];
+    double coef;
+    if (hm && hp) coef = 0.25 * kap * (1.0 / G[0].det + 1.0 / G[1].det);
+    else coef = kap / G[sref].det;
+    pen = eta * coef * W;
+    __syncthreads();
+  }
   // point coefficients: c_phi (value test) and c_g (normal-derivative test, along n)
   double cphi[2] = {0, 0}, cg[2] = {0, 0};
   if (mode == 0) {
@@ -303,20 +356,18 @@ k_dgface3(int mode, int axis, int bside, const double* __restrict__ x, double* _
       dnu[s] = a;
     }
     if (hm && hp) {
-      const double jump = u[0] - u[1];
       const double avg = 0.5 * (dnu[0] + dnu[1]);
-      cphi[0] = dS * (-avg + sigma * jump); cg[0] = -0.5 * dS * jump;
-      cphi[1] = dS * (avg - sigma * jump);  cg[1] = -0.5 * dS * jump;
+      cphi[0] = dS * (-avg + pen); cg[0] = -0.5 * dS * Jq;
+      cphi[1] = dS * (avg - pen);  cg[1] = -0.5 * dS * Jq;
     } else {
       const int s = sref;
-      cphi[s] = dS * (-dnu[s] + sigma * u[s]);
-      cg[s] = -dS * u[s];
+      cphi[s] = dS * (-dnu[s] + pen);
+      cg[s] = -dS * Jq;
     }
   } else {
     // boundary data g at this point: ordering (axis, side, elements ascending, points)
-    const double gv = gq[(long long)blockIdx.x * Q2 + tid];
-    cphi[sref] = dS * sigma * gv;
-    cg[sref] = -dS * gv;
+    cphi[sref] = dS * pen;
+    cg[sref] = -dS * Jq;
   }
   // transpose: reference-direction weights of the gradient test term
   for (int s = 0; s < 2; ++s) {
@@ -400,7 +451,7 @@ __global__ void k_bface_points(double* __restrict__ X, const double* __restrict_
 // diag(A_IP): volume |grad phi_a|^2 + faces (sigma phi^2 - c phi d_n phi), c = 1
 // interior, 2 boundary (written out from eq:ip; thread per DG dof; setup only)
 __global__ void k_dgdiag3(double* __restrict__ Dg, const double* __restrict__ V, const double* __restrict__ vol, int3 n,
-                          Basis1D bs, double eta) {
+                          Basis1D bs, double eta, int br2) {
   const int p = bs.p, Q = bs.q, NL = Q * Q * Q;
   const long long nel = (long long)n.x * n.y * n.z;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -441,11 +492,14 @@ __global__ void k_dgdiag3(double* __restrict__ Dg, const double* __restrict__ V,
       const bool interior = nb[k] >= 0 && nb[k] < nn[k];
       const double* E = side ? bs.E1 : bs.E0;
       const double sg = side ? 1.0 : -1.0;
-      double area = 0.0, s_pp = 0.0, s_pd = 0.0;
+      double area = 0.0, s_pp = 0.0, s_pd = 0.0, det_me = 1.0;
+      double beta[(MAXP + 1) * (MAXP + 1)];   // BR2: int_e phi_a psi_(i,j) dS on the face nodes
+      for (int i = 0; i < Q * Q; ++i) beta[i] = 0.0;
       for (int qj = 0; qj < Q; ++qj)
         for (int qi = 0; qi < Q; ++qi) {
           FaceGeo G;
           face_geo(V, n, ec, k, side, bs.xq[qi], bs.xq[qj], t1, t2, G, nullptr);
+          det_me = G.det;
           double nr = 0.0;
           for (int m = 0; m < 3; ++m) nr += G.Ji[k * 3 + m] * G.Ji[k * 3 + m];
           nr = sqrt(nr);
@@ -464,10 +518,35 @@ __global__ void k_dgdiag3(double* __restrict__ Dg, const double* __restrict__ V,
           area += dS;
           s_pp += dS * phi * phi;
           s_pd += dS * phi * dn;
+          if (br2)
+            for (int j = 0; j < Q; ++j)
+              for (int i = 0; i < Q; ++i) beta[i + Q * j] += dS * phi * bs.B[qi * Q + i] * bs.B[qj * Q + j];
         }
       const double hv = interior ? fmin(vol[e], vol[elem_id(nb, n)]) : vol[e];
-      const double sigma = eta / (hv / area);
-      acc += sigma * s_pp - (interior ? 1.0 : 2.0) * s_pd;
+      double pen;
+      if (!br2) {
+        pen = eta / (hv / area) * s_pp;
+      } else {
+        // eta sum_K s_K^2 b(phi_a)^T M_K^{-1} b(phi_a), affine M_K (see k_dgface3)
+        double quad = 0.0;
+        for (int j = 0; j < Q; ++j)
+          for (int i = 0; i < Q; ++i) {
+            double c = 0.0;
+            for (int j2 = 0; j2 < Q; ++j2)
+              for (int i2 = 0; i2 < Q; ++i2) c += bs.M1inv[i * Q + i2] * bs.M1inv[j * Q + j2] * beta[i2 + Q * j2];
+            quad += beta[i + Q * j] * c;
+          }
+        double inv_det = 1.0 / det_me;
+        double s2 = 1.0;
+        if (interior) {
+          FaceGeo Gn;
+          face_geo(V, n, nb, k, side ? 0 : 1, bs.xq[0], bs.xq[0], t1, t2, Gn, nullptr);
+          inv_det += 1.0 / Gn.det;
+          s2 = 0.25;
+        }
+        pen = eta * s2 * bs.M1inv[0] * inv_det * quad;
+      }
+      acc += pen - (interior ? 1.0 : 2.0) * s_pd;
     }
   Dg[t] = acc;
 }
@@ -525,7 +604,8 @@ static void launch_faces(const lorpc_mesh* m, const double* x, double* y, cudaSt
   const int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
   for (int k = 0; k < 3; ++k) {
     long long nf = (long long)(m->n[k] + 1) * (m->nel / m->n[k]);
-    k_dgface3<P><<<(unsigned)nf, Q * Q, 0, s>>>(0, k, 0, x, y, nullptr, m->V, m->vol, n, m->basis, m->desc.eta);
+    k_dgface3<P><<<(unsigned)nf, Q * Q, 0, s>>>(0, k, 0, x, y, nullptr, m->V, m->vol, n, m->basis, m->desc.eta,
+                                                 m->desc.disc == 2);
   }
 }
 template <int P, int EB>
@@ -563,7 +643,8 @@ int dg_diag_setup(lorpc_mesh* m, cudaStream_t s) {
   if (m->d != 3) return fail(LORPC_ERR_SIZE, "dg: 3D only");
   LORPC_TRY(dalloc(&m->dgdiag, (size_t)m->ndof));
   const int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
-  k_dgdiag3<<<(unsigned)((m->ndof + 127) / 128), 128, 0, s>>>(m->dgdiag, m->V, m->vol, n, m->basis, m->desc.eta);
+  k_dgdiag3<<<(unsigned)((m->ndof + 127) / 128), 128, 0, s>>>(m->dgdiag, m->V, m->vol, n, m->basis, m->desc.eta,
+                                                              m->desc.disc == 2);
   LORPC_LAUNCHED();
   std::vector<double> h(m->ndof);
   LORPC_CUDA(cudaMemcpyAsync(h.data(), m->dgdiag, sizeof(double) * m->ndof, cudaMemcpyDeviceToHost, s));
@@ -611,7 +692,7 @@ static void launch_bc(const lorpc_mesh* m, const double* gq, double* b, cudaStre
     for (int side = 0; side < 2; ++side) {
       const long long nf = m->nel / m->n[k];
       k_dgface3<P><<<(unsigned)nf, Q * Q, 0, s>>>(1, k, side, nullptr, b, gq + base, m->V, m->vol, n, m->basis,
-                                                 m->desc.eta);
+                                                 m->desc.eta, m->desc.disc == 2);
       base += nf * Q * Q;
     }
 }

@@ -138,3 +138,45 @@ def sipg_1d(p, n, sigma_c):
             av[(n - 1) * nl:] = dR
         A += -np.outer(jm, av) - np.outer(av, jm) + sigma * np.outer(jm, jm)
     return A, M
+
+
+def br2_1d(p, n, eta):
+    """1D BR2 (Gauss q=p+1) on n equal elements of [0,1], weak Dirichlet at both ends.
+    The lifting of a point jump into element K is r = -s_K M_K^{-1} (J n psi^K(x_e)),
+    so eta (r_e[u], r_e[v]) = eta J(u) J(v) sum_K s_K^2 (M_K^{-1})_{end,end}
+    (s = 1/2 interior, 1 boundary).  Built from the SIPG form with sigma replaced."""
+    xi = gll_nodes(p)
+    xg, wg = gauss(p + 1)
+    B, D = lagrange_tables(xi, xg)
+    e0, de0 = lagrange_tables(xi, np.array([0.0, 1.0]))
+    h = 1.0 / n
+    nl = p + 1
+    Mref = B.T @ np.diag(wg) @ B
+    Minv = np.linalg.inv(Mref * h)
+    A = np.zeros((n * nl, n * nl))
+    M = np.zeros((n * nl, n * nl))
+    for e in range(n):
+        s = slice(e * nl, (e + 1) * nl)
+        A[s, s] += D.T @ np.diag(wg) @ D / h
+        M[s, s] += Mref * h
+    vL, vR = e0[0], e0[1]
+    dL, dR = de0[0] / h, de0[1] / h
+    for f in range(n + 1):
+        jm = np.zeros(n * nl)
+        av = np.zeros(n * nl)
+        if 0 < f < n:
+            jm[(f - 1) * nl:f * nl] += vR
+            jm[f * nl:(f + 1) * nl] -= vL
+            av[(f - 1) * nl:f * nl] += 0.5 * dR
+            av[f * nl:(f + 1) * nl] += 0.5 * dL
+            pen = eta * 0.25 * (Minv[p, p] + Minv[0, 0])
+        elif f == 0:
+            jm[0:nl] = -vL
+            av[0:nl] = dL
+            pen = eta * Minv[0, 0]
+        else:
+            jm[(n - 1) * nl:] = vR
+            av[(n - 1) * nl:] = dR
+            pen = eta * Minv[p, p]
+        A += -np.outer(jm, av) - np.outer(av, jm) + pen * np.outer(jm, jm)
+    return A, M

@@ -1,0 +1,81 @@
+"""GPU-vs-oracle parity of the BR2 DG path (row a4): operator, weak-BC RHS,
+preconditioner (D_B includes the lifting diagonal) and PCG, on the C4 recipe."""
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import dirichlet_function, parity_vector, rhs_function, small_config, vertices
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1908_07071_b200 import lorpc
+    return lorpc
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# BR2 is coercive for eta above the number of element faces (2d = 6 in 3D); at
+# p = 5, eta = 1 the oracle reports a non-positive diag(A) entry, so the cases
+# use eta >= 10 (the GPU rejects it the same way, LORPC_ERR_ARG).
+CASES = [((3, 2, 3), 5, 10.0), ((2, 3, 2), 2, 10.0), ((3, 3, 2), 3, 1e3)]
+
+
+def _both(L, n, p, eta):
+    cfg = small_config("C4", n, p=p)
+    V = vertices(cfg)
+    return cfg, L.Mesh(3, cfg.n, cfg.p, V, disc=2, eta=eta), O.Problem(3, cfg.n, cfg.p, V, disc="br2", eta=eta)
+
+
+@pytest.mark.parametrize("n,p,eta", CASES)
+def test_br2_operator_and_rhs_parity(L, n, p, eta):
+    cfg, mesh, P = _both(L, n, p, eta)
+    x = parity_vector(P.ndof, seed=48)
+    y = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.apply(dev(x), y)
+    assert rel(y.cpu().numpy(), P.apply(x)) <= TOL
+    xq = torch.empty(mesh.n_quad * 3, dtype=torch.float64, device="cuda")
+    xb = torch.empty(mesh.n_bface_quad * 3, dtype=torch.float64, device="cuda")
+    mesh.quad_points(xq, xb)
+    Xo, Xbo = P.quad_points(), P.bface_points()
+    b = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    mesh.rhs_assemble(dev(rhs_function(cfg, Xo)), dev(dirichlet_function(cfg, Xbo)), b)
+    bo = P.rhs(rhs_function(cfg, Xo))
+    P.rhs_bc(dirichlet_function(cfg, Xbo), bo)
+    assert rel(b.cpu().numpy(), bo) <= TOL
+
+
+@pytest.mark.parametrize("n,p,eta", CASES)
+def test_br2_precond_and_pcg_parity(L, n, p, eta):
+    cfg, mesh, P = _both(L, n, p, eta)
+    prec = L.Prec(L.Lor(mesh))
+    P.schwarz_setup("vertex", "mdf", "gmg")
+    r = parity_vector(P.ndof, seed=49)
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    assert rel(z.cpu().numpy(), P.precond(r)) <= TOL
+    bo = P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty_like(z)
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, 1e-10)
+    xo, ro = P.pcg(bo, 1e-10)
+    assert abs(rep["iters"] - ro["iters"]) <= max(1, round(0.02 * ro["iters"]))
+    assert rel(x.cpu().numpy(), xo) <= 1e-8
+
+
+def test_br2_rejects_non_affine(L):
+    cfg = small_config("C5", (2, 2, 2))   # perturbed (trilinear) vertices
+    with pytest.raises(L.LorpcError) as e:
+        L.Mesh(3, cfg.n, cfg.p, vertices(cfg), disc=2, eta=1.0)
+    assert e.value.code == 2
