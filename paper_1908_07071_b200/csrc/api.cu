@@ -184,7 +184,7 @@ void lorpc_prec_destroy(lorpc_prec* b) {
     if (i > 0) dfree(b->Ac[i]);
     dfree(b->dl1[i]); dfree(b->cr[i]); dfree(b->cz[i]); dfree(b->cs[i]);
   }
-  dfree(b->coarse_chol); dfree(b->rcg); dfree(b->zcg); dfree(b->xb); dfree(b->wtab);
+  dfree(b->coarse_chol); dfree(b->rcg); dfree(b->zcg); dfree(b->xb); dfree(b->wtab); dfree(b->Cd);
   dfree(b->r); dfree(b->z); dfree(b->pv); dfree(b->qv); dfree(b->scal); dfree(b->part);
   if (b->hostpin) cudaFreeHost(b->hostpin);
   if (b->ev0) cudaEventDestroy(b->ev0);

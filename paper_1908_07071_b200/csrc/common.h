@@ -115,6 +115,9 @@ struct lorpc_prec {
   double* wtab = nullptr;
   int woff[lorpc::MAXL][4], wfe[lorpc::MAXL][4], wce[lorpc::MAXL][4];
   int scratch_doubles = 0;          // per-patch transfer scratch (V-cycle kernel)
+  int Ld = 0;                       // first level replaced by the dense coarse V-cycle operator
+  double* Cd = nullptr;             // [J][ldc] dense coarse operators (column-major n_Ld x n_Ld)
+  int ldc = 0;
   int lanes = 8;                    // lanes per patch in the V-cycle kernel
   // coarse space (R_0)
   int nc = 0;                       // GMG levels

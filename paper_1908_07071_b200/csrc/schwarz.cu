@@ -28,6 +28,7 @@ namespace lorpc {
 int galerkin(int d, const double* Af, double* Ac, const Transfer1D& T, const int* ne, const int* Nf, const int* Nc,
              cudaStream_t s);
 Transfer1D gmg_transfer();
+int dense_coarse_setup(lorpc_prec* b, cudaStream_t s);  // vcycle.cu
 
 // ------------------------------------------------------------------ MDF + ILU(0)
 __device__ __forceinline__ double q30(double x) {
@@ -510,6 +511,15 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
       LORPC_LAUNCHED();
     }
   }
+  // dense coarse V-cycle operators: first level l >= 1 with <= 32 free nodes per patch
+  // (the coarsest level if none); the V-cycle below it is one symmetric matrix
+  b->Ld = L - 1;
+  for (int l = 1; l < L; ++l)
+    if (b->max_n[l] <= 32) { b->Ld = l; break; }
+  if (b->max_n[b->Ld] > 64) return fail(LORPC_ERR_SIZE, "dense coarse level too large");
+  b->ldc = std::max(b->max_n[b->Ld] * b->max_n[b->Ld], 1);
+  LORPC_TRY(dalloc(&b->Cd, (size_t)b->J * b->ldc));
+  LORPC_TRY(dense_coarse_setup(b, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
   return LORPC_OK;
 }

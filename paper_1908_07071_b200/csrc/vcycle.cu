@@ -174,67 +174,69 @@ __global__ void k_coarsest_solve(const double* __restrict__ F, const double* __r
 
 
 // ------------------------------------------------------------------ patch V-cycle
-// Lane-group kernel: G lanes per patch, 32/G patches per warp (the level
-// schedules of MDF-ordered ILU(0) on 3D patches hold ~3-5 rows per DAG level,
-// so a full warp per patch left ~90% of the lanes idle; ncu r01).  Per patch the
-// shared memory holds the level vectors r_l, z_l, s_l and a transfer scratch;
-// the ILU records are read through L1/L2; the level operators A_l are read
-// row-major (AoS, 3^d contiguous doubles per node).
+// One warp per patch (G = 32 lanes).  Shared memory per patch: the level vectors
+// [r_l | z_l | s_l] for the finest levels, [r | z] at the dense level Ld, and a
+// transfer scratch, all addressed by 32-bit offsets into the dynamic array.
+// The ILU records are read with __ldg; the level operators A_l row-major.
+// Levels >= Ld (<= 32 free nodes per patch) are replaced by one precomputed dense
+// symmetric matrix per patch: the exact operator of the V-cycle restricted to
+// those levels (built by k_dense_coarse from the same ILU records), so the whole
+// coarse part of the cycle is one matrix-vector product.
+extern __shared__ __align__(16) double vsm[];
+
 struct VcParams {
   PatchGeom G;
   const double* A[MAXL];
   const double* W;        // separable 1D restriction tables (host-built, see schwarz.cu)
   int woff[MAXL][4];      // table offset for (level l -> l+1, elements along the axis 1..3)
-  int wfe[MAXL][4];       // fine extent of that table
-  int wce[MAXL][4];       // coarse extent
   const char* rec;
   const long long* recoff;
   long long J;
+  int Ld;                 // first level covered by the dense coarse operator
+  double* Cd;             // [J][ldc] column-major n_Ld x n_Ld dense coarse V-cycle operators
+  int ldc;
   int soff[MAXL];         // per-patch SMEM offsets (doubles) of [r | z | s] at level l
   int nmax[MAXL];
   int toff;               // transfer scratch offset
-  int roff;               // staged record offset (doubles), rec_doubles long
-  int rec_doubles;
-  int boff;               // mbarrier offset (doubles)
-  long long rec_total;
   int patch_doubles;
   const double* r;
   double* z;
 };
 
-// One DAG level of a triangular sweep by the G lanes of a group: the level's
-// entries [eb, ee) are contiguous; each lane multiplies one entry, a segmented
-// shuffle reduction sums each row's entries (rows are contiguous, slots
-// non-decreasing), and the row's first lane subtracts the sum.  Rows of one level
-// are independent, so chunks need no synchronisation between them.
-template <int G>
-__device__ __forceinline__ void seg_level(const double* L, const uint16_t* col, const uint16_t* pos,
-                                          const uint8_t* sg, const uint16_t* sch, int eb, int ee, int rb,
-                                          double* v, int gl, unsigned gmask) {
-  for (int c0 = eb; c0 < ee; c0 += G) {
-    const int q = c0 + gl;
+// One DAG level of a triangular sweep: the level's entries [eb, ee) are contiguous;
+// each lane multiplies one entry, a segmented shuffle reduction sums each row's
+// entries (rows contiguous in the level; the row starts of a chunk come from one
+// ballot), and the row's first lane subtracts the sum.  Rows of one level are
+// independent, so chunks need no synchronisation between them.  v is a 32-bit
+// offset into shared memory.
+__device__ __forceinline__ void seg_level(const double* __restrict__ L, const uint16_t* __restrict__ col,
+                                          const uint16_t* __restrict__ pos, const uint8_t* __restrict__ sg,
+                                          const uint16_t* __restrict__ sch, int eb, int ee, int rb, int v, int lane) {
+  for (int c0 = eb; c0 < ee; c0 += 32) {
+    const int q = c0 + lane;
     const bool in = q < ee;
     double val = 0.0;
-    int seg = 1024 + gl;
-    if (in) { val = __ldg(L + (pos ? __ldg(pos + q) : q)) * v[__ldg(col + q)]; seg = __ldg(sg + q); }
+    int seg = -1;
+    if (in) { val = __ldg(L + (pos ? __ldg(pos + q) : q)) * vsm[v + __ldg(col + q)]; seg = __ldg(sg + q); }
+    const int ps = __shfl_up_sync(0xffffffffu, seg, 1);
+    const bool head = in && (lane == 0 || ps != seg);
+    const unsigned heads = __ballot_sync(0xffffffffu, head) | ~__ballot_sync(0xffffffffu, in);
+    // lanes (lane, lane+off] hold no row start  <=>  same row
+    const unsigned above = heads >> lane >> 1;
 #pragma unroll
-    for (int off = 1; off < G; off <<= 1) {
-      const double ov = __shfl_down_sync(gmask, val, off, G);
-      const int os = __shfl_down_sync(gmask, seg, off, G);
-      if (gl + off < G && os == seg) val += ov;
+    for (int off = 1; off < 32; off <<= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, val, off);
+      if ((above & ((1u << off) - 1u)) == 0u && lane + off < 32) val += ov;
     }
-    const int ps = __shfl_up_sync(gmask, seg, 1, G);
-    if (in && (gl == 0 || ps != seg)) v[__ldg(sch + rb + seg)] -= val;
+    if (head) vsm[v + __ldg(sch + rb + seg)] -= val;
   }
 }
 
 // v := M^{-1} v, M = L D L^T of one patch level (forward L, diagonal, backward L^T)
-template <int G>
-__device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int gl) {
+__device__ __forceinline__ void ilu_w(const char* __restrict__ rec, bool act, int v, int lane) {
   int n = 0, depth = 0, nL = 0;
   if (act) { const int4 h = __ldg((const int4*)rec); n = h.x; depth = h.y; nL = h.z; }
-  const int md = __reduce_max_sync(0xffffffffu, depth);
-  if (md == 0) return;
+  if (depth == 0) return;
   const RecLayout R = rec_layout(n, nL);
   const double* D = (const double*)(rec + R.D);
   const double* L = (const double*)(rec + R.L);
@@ -247,233 +249,246 @@ __device__ __forceinline__ void ilu_g(const char* rec, bool act, double* v, int 
   const uint16_t* belv = (const uint16_t*)(rec + R.belev);
   const uint16_t* lpt = (const uint16_t*)(rec + R.lptr);
   const uint16_t* sch = (const uint16_t*)(rec + R.sched);
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (((threadIdx.x & 31) / G) * G));
-  for (int lv = 0; lv < md; ++lv) {
-    if (lv < depth)
-      seg_level<G>(L, nb, nullptr, sg, sch, __ldg(elv + lv), __ldg(elv + lv + 1), __ldg(lpt + lv), v, gl, gmask);
+  for (int lv = 0; lv < depth; ++lv) {
+    seg_level(L, nb, nullptr, sg, sch, __ldg(elv + lv), __ldg(elv + lv + 1), __ldg(lpt + lv), v, lane);
     __syncwarp();
   }
-  for (int i = gl; i < n; i += G) v[i] = v[i] / __ldg(D + i);
+  for (int i = lane; i < n; i += 32) vsm[v + i] = vsm[v + i] / __ldg(D + i);
   __syncwarp();
-  for (int lv = md - 1; lv >= 0; --lv) {
-    if (lv < depth)
-      seg_level<G>(L, bk, bp, bsg, sch, __ldg(belv + lv), __ldg(belv + lv + 1), __ldg(lpt + lv), v, gl, gmask);
+  for (int lv = depth - 1; lv >= 0; --lv) {
+    seg_level(L, bk, bp, bsg, sch, __ldg(belv + lv), __ldg(belv + lv + 1), __ldg(lpt + lv), v, lane);
     __syncwarp();
   }
 }
 
 // s = r - A_l z on the patch box (A_l row-major: ND contiguous doubles per node)
-template <int DIM, int G>
-__device__ __forceinline__ void residual_g(const double* __restrict__ A, long long Nx, long long Ny, const int* lo,
-                                           const int* ext, const double* r, const double* z, double* s, int n, int gl) {
+template <int DIM>
+__device__ __forceinline__ void residual_w(const double* __restrict__ A, long long Nx, long long Ny, const int* lo,
+                                           const int* ext, int r, int z, int s, int lane) {
   constexpr int ND = Dirs<DIM>::ND;
-  const int ex = ext[0], ey = ext[1], ez = ext[2];
+  const int ex = ext[0], ey = ext[1], ez = ext[2], n = ex * ey * ez;
   const float rex = 1.0f / ex, rexy = 1.0f / (ex * ey);
-  for (int i = gl; i < n; i += G) {
+  for (int i = lane; i < n; i += 32) {
     int ix, iy, iz;
     box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
     const long long gi = (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0));
     const double* Ar = A + gi * ND;
     const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
-    double a0 = r[i], a1 = 0.0;
+    double a0 = vsm[r + i], a1 = 0.0;
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
-      const double zv = (em & (1u << d)) ? z[i + doff<DIM>(d, ex, ey)] : 0.0;
+      const double zv = (em & (1u << d)) ? vsm[z + i + doff<DIM>(d, ex, ey)] : 0.0;
       const double t2 = __ldg(Ar + d) * zv;
       if (d & 1) a1 += t2; else a0 -= t2;
     }
-    s[i] = a0 - a1;
+    vsm[s + i] = a0 - a1;
   }
 }
 
-template <int DIM, int G>
-__global__ void __launch_bounds__(128, LORPC_VC_MINB) k_vcycle(VcParams P) {
-  constexpr int PPW = 32 / G;
-  extern __shared__ __align__(16) double sm[];
-  const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
-  const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (wg * PPW >= P.J) return;  // warp-uniform
-  const long long j = wg * PPW + grp;
-  const bool act = j < P.J;
-  double* W = sm + (long long)((threadIdx.x >> 5) * PPW + grp) * P.patch_doubles;
-  const int L = P.G.L;
-  int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
-  if (act) patch_elems(P.G, j, elo, ehi);
-  int ec[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) ec[k] = ehi[k] - elo[k] + 1;
-  auto box = [&](int l, int* lo, int* ext) {
-    const int m = P.G.ml[l];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (k >= DIM) { lo[k] = 0; ext[k] = 1; continue; }
-      lo[k] = elo[k] * (m - 1) + 1;
-      ext[k] = act ? ec[k] * (m - 1) - 1 : 0;
-    }
-  };
-  auto rv = [&](int l) { return W + P.soff[l]; };
-  auto zv = [&](int l) { return W + P.soff[l] + P.nmax[l]; };
-  auto sv = [&](int l) { return W + P.soff[l] + 2 * P.nmax[l]; };
-  // ---- stage this patch's ILU records (all levels, contiguous, 16 B aligned) in
-  // shared memory with one TMA bulk copy (cp.async.bulk + mbarrier transaction count)
-  const long long rb0 = act ? P.recoff[j * L] : 0;
-  const long long rb1 = act ? ((j + 1 < P.J) ? P.recoff[(j + 1) * L] : P.rec_total) : 0;
-  char* srec = (char*)(W + P.roff);
-  {
-    uint64_t* bar = (uint64_t*)(W + P.boff);
-    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bar);
-    const unsigned dst_s = (unsigned)__cvta_generic_to_shared(srec);
-    const unsigned bytes = (unsigned)(rb1 - rb0);
-    if (P.rec_doubles == 0) srec = (char*)(P.rec + rb0);   // records read through L1/L2
-    else if (act && gl == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s) : "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
-          "l"(P.rec + rb0), "r"(bytes), "r"(bar_s)
-          : "memory");
-    }
-    __syncwarp();
-    if (act && P.rec_doubles > 0) {
-      unsigned done = 0;
-      while (!done) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(bar_s)
-            : "memory");
-      }
-    }
-  }
-  auto recl = [&](int l) { return (const char*)srec + (act ? P.recoff[j * L + l] - rb0 : 0); };
-  double* T1 = W + P.toff;
-  // ---- gather r_j = I_j^T r (a5)
-  {
-    int lo[3], ext[3];
-    box(0, lo, ext);
-    const int n = ext[0] * ext[1] * ext[2];
-    const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-    double* r0 = rv(0);
-    const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
-    for (int i = gl; i < n; i += G) {
-      int ix, iy, iz;
-      box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
-      r0[i] = __ldg(P.r + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)));
-    }
+// rc = P^T s (separable: x, y, z passes through the scratch T at offset t)
+template <int DIM>
+__device__ __forceinline__ void restrict_w(const double* Wx, const double* Wy, const double* Wz, const int* ext,
+                                           const int* cext, int s, int rc, int t, int lane) {
+  const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
+  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy);
+  const int T2 = DIM == 3 ? t + cx * fy * fz : rc;
+  for (int u = lane; u < cx * fy * fz; u += 32) {
+    const int rest = qdiv(u, rcx), ic = u - rest * cx;
+    double a = 0.0;
+    for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * vsm[s + f + fx * rest];
+    vsm[t + u] = a;
   }
   __syncwarp();
-  // ---- downward leg: pre-smooth, residual, restrict (separable P^T)
-  for (int l = 0; l < L - 1; ++l) {
-    int lo[3], ext[3], clo[3], cext[3];
-    box(l, lo, ext);
-    box(l + 1, clo, cext);
-    const int n = ext[0] * ext[1] * ext[2];
-    double *r = rv(l), *z = zv(l), *s = sv(l);
-    for (int i = gl; i < n; i += G) z[i] = r[i];
-    __syncwarp();
-    ilu_g<G>(recl(l), act, z, gl);
-    residual_g<DIM, G>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, r, z, s, n, gl);
-    __syncwarp();
-    const double* Wx = P.W + P.woff[l][ec[0]];
-    const double* Wy = P.W + P.woff[l][ec[1]];
-    const double* Wz = P.W + P.woff[l][DIM == 3 ? ec[2] : 1];
-    const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
-    double* rc = rv(l + 1);
-    double* T2 = DIM == 3 ? T1 + cx * fy * fz : rc;
-    const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
-    for (int t = gl; t < cx * fy * fz; t += G) {           // x pass
-      const int rest = qdiv(t, rcx), ic = t - rest * cx;
-      double a = 0.0;
-      for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * s[f + fx * rest];
-      T1[t] = a;
-    }
-    __syncwarp();
-    for (int t = gl; t < cx * cy * fz; t += G) {           // y pass
-      const int kf = qdiv(t, rcxy), r2 = t - kf * cx * cy, jc = qdiv(r2, rcx), ic = r2 - jc * cx;
-      double a = 0.0;
-      for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * T1[ic + cx * (f + fy * kf)];
-      T2[t] = a;
-    }
-    __syncwarp();
-    if (DIM == 3) {
-      for (int t = gl; t < cx * cy * cz; t += G) {         // z pass
-        const int kc = qdiv(t, rcxy), ij = t - kc * cx * cy;
-        double a = 0.0;
-        for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * T2[ij + cx * cy * f];
-        rc[t] = a;
-      }
-      __syncwarp();
-    }
+  for (int u = lane; u < cx * cy * fz; u += 32) {
+    const int kf = qdiv(u, rcxy), r2 = u - kf * cx * cy, jc = qdiv(r2, rcx), ic = r2 - jc * cx;
+    double a = 0.0;
+    for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * vsm[t + ic + cx * (f + fy * kf)];
+    vsm[T2 + u] = a;
   }
-  // ---- coarsest level: exact LDL^T (reading c8)
+  __syncwarp();
+  if (DIM == 3) {
+    for (int u = lane; u < cx * cy * cz; u += 32) {
+      const int kc = qdiv(u, rcxy), ij = u - kc * cx * cy;
+      double a = 0.0;
+      for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * vsm[T2 + ij + cx * cy * f];
+      vsm[rc + u] = a;
+    }
+    __syncwarp();
+  }
+}
+
+// z += P e (separable transpose of restrict_w)
+template <int DIM>
+__device__ __forceinline__ void prolong_w(const double* Wx, const double* Wy, const double* Wz, const int* ext,
+                                          const int* cext, int e, int z, int t, int lane) {
+  const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
+  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
+  int U2 = e;
+  if (DIM == 3) {
+    U2 = t + cx * fy * fz;
+    for (int u = lane; u < cx * cy * fz; u += 32) {          // z pass: [cx][cy][fz]
+      const int kf = qdiv(u, rcxy), ij = u - kf * cx * cy;
+      double a = 0.0;
+      for (int c = 0; c < cz; ++c) a += __ldg(Wz + c * fz + kf) * vsm[e + ij + cx * cy * c];
+      vsm[U2 + u] = a;
+    }
+    __syncwarp();
+  }
+  for (int u = lane; u < cx * fy * fz; u += 32) {            // y pass: [cx][fy][fz]
+    const int kf = qdiv(u, rcxfy), r2 = u - kf * cx * fy, jf = qdiv(r2, rcx), ic = r2 - jf * cx;
+    double a = 0.0;
+    for (int c = 0; c < cy; ++c) a += __ldg(Wy + c * fy + jf) * vsm[U2 + ic + cx * (c + cy * kf)];
+    vsm[t + u] = a;
+  }
+  __syncwarp();
+  const int n = fx * fy * fz;
+  for (int i = lane; i < n; i += 32) {                        // x pass, z += P e
+    const int rest = qdiv(i, rfx), fxi = i - rest * fx;
+    double a = 0.0;
+    for (int c = 0; c < cx; ++c) a += __ldg(Wx + c * fx + fxi) * vsm[t + c + cx * rest];
+    vsm[z + i] += a;
+  }
+  __syncwarp();
+}
+
+// Patch geometry of one warp's patch
+struct PatchCtx {
+  int elo[3], ec[3];
+  bool act;
+};
+template <int DIM>
+__device__ __forceinline__ void box_of(const VcParams& P, const PatchCtx& c, int l, int* lo, int* ext) {
+  const int m = P.G.ml[l];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= DIM) { lo[k] = 0; ext[k] = 1; continue; }
+    lo[k] = c.elo[k] * (m - 1) + 1;
+    ext[k] = c.act ? c.ec[k] * (m - 1) - 1 : 0;
+  }
+}
+
+// V(1,1) over levels l0..l1-1 with ILU smoothing; at level l1 either the dense
+// operator (dense = true) or the ILU record (an exact solve at the coarsest level).
+// Input r_{l0} at soff[l0], output z_{l0} at soff[l0] + nmax[l0].
+template <int DIM>
+__device__ void vcycle_range(const VcParams& P, const PatchCtx& c, long long j, int base, int l0, int l1, bool dense,
+                             int lane) {
+  const int L = P.G.L;
+  auto rv = [&](int l) { return base + P.soff[l]; };
+  auto zv = [&](int l) { return base + P.soff[l] + P.nmax[l]; };
+  auto sv = [&](int l) { return base + P.soff[l] + 2 * P.nmax[l]; };
+  auto recl = [&](int l) { return P.rec + (c.act ? P.recoff[j * L + l] : 0); };
+  const int T = base + P.toff;
+  for (int l = l0; l < l1; ++l) {
+    int lo[3], ext[3], clo[3], cext[3];
+    box_of<DIM>(P, c, l, lo, ext);
+    box_of<DIM>(P, c, l + 1, clo, cext);
+    const int n = ext[0] * ext[1] * ext[2];
+    for (int i = lane; i < n; i += 32) vsm[zv(l) + i] = vsm[rv(l) + i];
+    __syncwarp();
+    ilu_w(recl(l), c.act, zv(l), lane);                       // pre-smoothing
+    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, rv(l), zv(l), sv(l), lane);
+    __syncwarp();
+    restrict_w<DIM>(P.W + P.woff[l][c.ec[0]], P.W + P.woff[l][c.ec[1]], P.W + P.woff[l][DIM == 3 ? c.ec[2] : 1],
+                    ext, cext, sv(l), rv(l + 1), T, lane);
+  }
   {
     int lo[3], ext[3];
-    box(L - 1, lo, ext);
+    box_of<DIM>(P, c, l1, lo, ext);
     const int n = ext[0] * ext[1] * ext[2];
-    double *r = rv(L - 1), *z = zv(L - 1);
-    for (int i = gl; i < n; i += G) z[i] = r[i];
-    __syncwarp();
-    ilu_g<G>(recl(L - 1), act, z, gl);
-  }
-  // ---- upward leg: prolongate (separable P), residual, post-smooth
-  for (int l = L - 2; l >= 0; --l) {
-    int lo[3], ext[3], clo[3], cext[3];
-    box(l, lo, ext);
-    box(l + 1, clo, cext);
-    const int n = ext[0] * ext[1] * ext[2];
-    double *r = rv(l), *z = zv(l), *s = sv(l);
-    const double* e = zv(l + 1);
-    const double* Wx = P.W + P.woff[l][ec[0]];
-    const double* Wy = P.W + P.woff[l][ec[1]];
-    const double* Wz = P.W + P.woff[l][DIM == 3 ? ec[2] : 1];
-    const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
-    const double* U2 = e;
-    const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
-    if (DIM == 3) {
-      double* U2w = T1 + cx * fy * fz;
-      for (int t = gl; t < cx * cy * fz; t += G) {         // z pass: [cx][cy][fz]
-        const int kf = qdiv(t, rcxy), ij = t - kf * cx * cy;
-        double a = 0.0;
-        for (int c = 0; c < cz; ++c) a += __ldg(Wz + c * fz + kf) * e[ij + cx * cy * c];
-        U2w[t] = a;
+    if (dense) {                                              // z = C r (column-major, symmetric)
+      const double* C = P.Cd + (c.act ? j : 0) * (long long)P.ldc;
+      for (int i = lane; i < n; i += 32) {
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 1 < n; k += 2) {
+          a0 += __ldg(C + (long long)k * n + i) * vsm[rv(l1) + k];
+          a1 += __ldg(C + (long long)(k + 1) * n + i) * vsm[rv(l1) + k + 1];
+        }
+        if (k < n) a0 += __ldg(C + (long long)k * n + i) * vsm[rv(l1) + k];
+        vsm[zv(l1) + i] = a0 + a1;
       }
       __syncwarp();
-      U2 = U2w;
+    } else {
+      for (int i = lane; i < n; i += 32) vsm[zv(l1) + i] = vsm[rv(l1) + i];
+      __syncwarp();
+      ilu_w(recl(l1), c.act, zv(l1), lane);
     }
-    for (int t = gl; t < cx * fy * fz; t += G) {           // y pass: [cx][fy][fz]
-      const int kf = qdiv(t, rcxfy), r2 = t - kf * cx * fy, jf = qdiv(r2, rcx), ic = r2 - jf * cx;
-      double a = 0.0;
-      for (int c = 0; c < cy; ++c) a += __ldg(Wy + c * fy + jf) * U2[ic + cx * (c + cy * kf)];
-      T1[t] = a;
-    }
+  }
+  for (int l = l1 - 1; l >= l0; --l) {
+    int lo[3], ext[3], clo[3], cext[3];
+    box_of<DIM>(P, c, l, lo, ext);
+    box_of<DIM>(P, c, l + 1, clo, cext);
+    const int n = ext[0] * ext[1] * ext[2];
+    prolong_w<DIM>(P.W + P.woff[l][c.ec[0]], P.W + P.woff[l][c.ec[1]], P.W + P.woff[l][DIM == 3 ? c.ec[2] : 1],
+                   ext, cext, zv(l + 1), zv(l), T, lane);
+    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, rv(l), zv(l), sv(l), lane);
     __syncwarp();
-    for (int i = gl; i < n; i += G) {                      // x pass, z += P e
-      const int rest = qdiv(i, rfx), fxi = i - rest * fx;
-      double a = 0.0;
-      for (int c = 0; c < cx; ++c) a += __ldg(Wx + c * fx + fxi) * T1[c + cx * rest];
-      z[i] += a;
-    }
-    __syncwarp();
-    residual_g<DIM, G>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, r, z, s, n, gl);
-    __syncwarp();
-    ilu_g<G>(recl(l), act, s, gl);
-    for (int i = gl; i < n; i += G) z[i] += s[i];
+    ilu_w(recl(l), c.act, sv(l), lane);                       // post-smoothing
+    for (int i = lane; i < n; i += 32) vsm[zv(l) + i] += vsm[sv(l) + i];
     __syncwarp();
   }
-  // ---- z += I_j z_j (a8)
-  {
-    int lo[3], ext[3];
-    box(0, lo, ext);
-    const int n = ext[0] * ext[1] * ext[2];
-    const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-    const double* z0 = zv(0);
-    const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
-    for (int i = gl; i < n; i += G) {
-      int ix, iy, iz;
-      box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
-      atomicAdd(P.z + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)), z0[i]);
-    }
+}
+
+template <int DIM>
+__device__ __forceinline__ PatchCtx patch_ctx(const VcParams& P, long long j) {
+  PatchCtx c;
+  c.act = j < P.J;
+  int ehi[3] = {0, 0, 0};
+  c.elo[0] = c.elo[1] = c.elo[2] = 0;
+  if (c.act) patch_elems(P.G, j, c.elo, ehi);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c.ec[k] = ehi[k] - c.elo[k] + 1;
+  return c;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128, LORPC_VC_MINB) k_vcycle(VcParams P) {
+  const int lane = threadIdx.x & 31;
+  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (j >= P.J) return;  // warp-uniform
+  const int base = (threadIdx.x >> 5) * P.patch_doubles;
+  const PatchCtx c = patch_ctx<DIM>(P, j);
+  int lo[3], ext[3];
+  box_of<DIM>(P, c, 0, lo, ext);
+  const int n = ext[0] * ext[1] * ext[2];
+  const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+  const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
+  for (int i = lane; i < n; i += 32) {                        // r_j = I_j^T r (a5)
+    int ix, iy, iz;
+    box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
+    vsm[base + P.soff[0] + i] = __ldg(P.r + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)));
+  }
+  __syncwarp();
+  vcycle_range<DIM>(P, c, j, base, 0, P.Ld, true, lane);
+  const int z0 = base + P.soff[0] + P.nmax[0];
+  for (int i = lane; i < n; i += 32) {                        // z += I_j z_j (a8)
+    int ix, iy, iz;
+    box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
+    atomicAdd(P.z + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)), vsm[z0 + i]);
+  }
+}
+
+// setup: dense operator of the V-cycle on levels Ld..L-1 for every patch (columns
+// = images of the unit vectors), one warp per patch
+template <int DIM>
+__global__ void __launch_bounds__(128) k_dense_coarse(VcParams P) {
+  const int lane = threadIdx.x & 31;
+  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (j >= P.J) return;
+  const int base = (threadIdx.x >> 5) * P.patch_doubles;
+  const PatchCtx c = patch_ctx<DIM>(P, j);
+  const int Ld = P.Ld, L = P.G.L;
+  int lo[3], ext[3];
+  box_of<DIM>(P, c, Ld, lo, ext);
+  const int n = ext[0] * ext[1] * ext[2];
+  double* C = P.Cd + j * (long long)P.ldc;
+  for (int k = 0; k < n; ++k) {
+    for (int i = lane; i < n; i += 32) vsm[base + P.soff[Ld] + i] = (i == k) ? 1.0 : 0.0;
+    __syncwarp();
+    vcycle_range<DIM>(P, c, j, base, Ld, L - 1, false, lane);
+    for (int i = lane; i < n; i += 32) C[(long long)k * n + i] = vsm[base + P.soff[Ld] + P.nmax[Ld] + i];
+    __syncwarp();
   }
 }
 
@@ -528,62 +543,56 @@ __global__ void k_zero_dir(double* z, int3 N) {
   if (dd) z[g] = 0.0;
 }
 
-template <int DIM, int G>
-static int launch_vcycle(const VcParams& P, long long J, cudaStream_t s) {
-  constexpr int PPW = 32 / G;
-  const size_t per_warp = (size_t)PPW * P.patch_doubles * sizeof(double);
-  int wpb = 4;
-  while (wpb > 1 && per_warp * wpb > 113 * 1024) wpb >>= 1;
-  const size_t smem = per_warp * wpb;
-  if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle: patch does not fit in shared memory");
-  const long long warps = (J + PPW - 1) / PPW;
-  const unsigned blocks = (unsigned)((warps + wpb - 1) / wpb);
-  cudaFuncSetAttribute(k_vcycle<DIM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_vcycle<DIM, G><<<blocks, 32 * wpb, smem, s>>>(P);
-  LORPC_LAUNCHED();
-  return LORPC_OK;
-}
-
-int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
-  const lorpc_mesh* m = b->m;
+static VcParams make_params(const lorpc_prec* b, const double* r, double* z) {
   const lorpc_lor* lor = b->lor;
-  const int d = m->d, L = b->L;
-  LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * m->ndof_cg, s));
+  const int L = b->L;
   VcParams P{};
   P.G = make_geom(b);
   for (int l = 0; l < L; ++l) P.A[l] = lor->A[l];
   P.W = b->wtab;
   memcpy(P.woff, b->woff, sizeof(P.woff));
-  memcpy(P.wfe, b->wfe, sizeof(P.wfe));
-  memcpy(P.wce, b->wce, sizeof(P.wce));
   P.rec = b->rec; P.recoff = b->recoff; P.J = b->J; P.r = r; P.z = z;
+  P.Ld = b->Ld; P.Cd = b->Cd; P.ldc = b->ldc;
   int acc = 0;
   for (int l = 0; l < L; ++l) { P.soff[l] = acc; P.nmax[l] = b->max_n[l]; acc += 3 * b->max_n[l]; }
   P.toff = acc;
   acc += b->scratch_doubles;
-  acc = (acc + 1) & ~1;                 // 16-byte alignment of the staged record
-  P.roff = acc;
-  // Patch records are read through L1/L2 (LORPC_STAGE=1 stages each patch's records
-  // in shared memory with one TMA bulk copy; measured slower: SMEM caps the warps).
-  const bool stage = false;  // records are read with __ldg: the staged variant is retired
-  P.rec_doubles = stage ? (int)(b->rec_max / 8) : 0;
-  acc += P.rec_doubles;
-  P.boff = acc;                         // mbarrier
-  acc += 2;
-  P.patch_doubles = acc;
-  P.rec_total = b->rec_bytes;
-  int G = b->lanes;
+  P.patch_doubles = (acc + 1) & ~1;
+  return P;
+}
+
+template <int DIM, bool SETUP>
+static int launch_vc(const VcParams& P, long long J, cudaStream_t s) {
+  const size_t per_warp = (size_t)P.patch_doubles * sizeof(double);
+  const int wpb = 4;
+  const size_t smem = per_warp * wpb;
+  if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle: patch does not fit in shared memory");
+  const unsigned blocks = (unsigned)((J + wpb - 1) / wpb);
+  if (SETUP) {
+    cudaFuncSetAttribute(k_dense_coarse<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_dense_coarse<DIM><<<blocks, 32 * wpb, smem, s>>>(P);
+  } else {
+    cudaFuncSetAttribute(k_vcycle<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_vcycle<DIM><<<blocks, 32 * wpb, smem, s>>>(P);
+  }
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+
+int dense_coarse_setup(lorpc_prec* b, cudaStream_t s) {
+  VcParams P = make_params(b, nullptr, nullptr);
+  return b->m->d == 2 ? launch_vc<2, true>(P, b->J, s) : launch_vc<3, true>(P, b->J, s);
+}
+
+int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  const lorpc_mesh* m = b->m;
+  const int d = m->d;
+  LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * m->ndof_cg, s));
+  VcParams P = make_params(b, r, z);
   lorpc_prec* bm = const_cast<lorpc_prec*>(b);
   const bool prof = bm->prof_on && bm->prof_n < (int)bm->prof_ev.size() / 2;
   if (prof) LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n], s));
-  int rc;
-  if (d == 2) {
-    rc = G == 4 ? launch_vcycle<2, 4>(P, b->J, s) : G == 8 ? launch_vcycle<2, 8>(P, b->J, s)
-       : G == 16 ? launch_vcycle<2, 16>(P, b->J, s) : launch_vcycle<2, 32>(P, b->J, s);
-  } else {
-    rc = G == 4 ? launch_vcycle<3, 4>(P, b->J, s) : G == 8 ? launch_vcycle<3, 8>(P, b->J, s)
-       : G == 16 ? launch_vcycle<3, 16>(P, b->J, s) : launch_vcycle<3, 32>(P, b->J, s);
-  }
+  const int rc = d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
   if (rc != LORPC_OK) return rc;
   if (prof) { LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n + 1], s)); bm->prof_n++; }
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
