@@ -72,28 +72,27 @@ __host__ __device__ __forceinline__ long long a8(long long b) { return (b + 7) &
 // once, in forward-solve order: grouped by DAG level of the triangular solve,
 // within a level by row (schedule order), within a row by direction:
 //   D[n]        pivots (natural index)
-//   L[nL]       L_ij, row i = sched[lptr[lv] + seg], column j = nb
-//   nb[nL]      natural index j (u16)
-//   sg[nL]      row slot within its DAG level (u8)
-//   elev[n+1]   entry offset of each DAG level
-//   lptr[n+1]   row offset of each DAG level into sched
-//   sched[n]    rows in schedule order (natural index)
+//   L[nL]       L_ij of the forward sweep
+//   nb[nL]      column j (natural index, u16)
+//   rw[nL]      row i (natural index, u16): the segment key of the row reduction
+//   bL, bk, brw [nL]: the backward (L^T) entries, grouped the same way by DAG level
+//     and row i: value L_ki (duplicated so that no load depends on another), upper
+//     neighbour k, row i
+//   elev[n+1], belev[n+1]  entry offset of each DAG level (forward / backward)
+//   lptr[n+1], sched[n]    DAG level row pointers / rows in schedule order (setup)
 //   order[n]    elimination order (export only)
-//   bk[nL], bp[nL], bsg[nL], belev[n+1]: the backward (L^T) entries, grouped the
-//     same way by DAG level and row i: upper neighbour k, position of L_ki in L,
-//     row slot of i within its level
 // Both sweeps pull, with a segmented warp reduction per row (deterministic).
-struct RecLayout { long long D, L, nb, sg, bk, bp, bsg, elev, belev, lptr, sched, order, total; };
+struct RecLayout { long long D, L, nb, rw, bL, bk, brw, elev, belev, lptr, sched, order, total; };
 __host__ __device__ __forceinline__ RecLayout rec_layout(int n, long long nL) {
   RecLayout R;
   R.D = 16;
   R.L = R.D + 8ll * n;
   R.nb = R.L + 8ll * nL;
-  R.sg = R.nb + a8(2ll * nL);
-  R.bk = R.sg + a8(nL);
-  R.bp = R.bk + a8(2ll * nL);
-  R.bsg = R.bp + a8(2ll * nL);
-  R.elev = R.bsg + a8(nL);
+  R.rw = R.nb + a8(2ll * nL);
+  R.bL = R.rw + a8(2ll * nL);
+  R.bk = R.bL + 8ll * nL;
+  R.brw = R.bk + a8(2ll * nL);
+  R.elev = R.brw + a8(2ll * nL);
   R.belev = R.elev + a8(2ll * (n + 1));
   R.lptr = R.belev + a8(2ll * (n + 1));
   R.sched = R.lptr + a8(2ll * (n + 1));

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
     double* Dr = (double*)(rec + R.D);
     double* Lr = (double*)(rec + R.L);
     uint16_t* nbr = (uint16_t*)(rec + R.nb);
-    uint8_t* sgr = (uint8_t*)(rec + R.sg);
+    uint16_t* rwr = (uint16_t*)(rec + R.rw);
     uint16_t* elv = (uint16_t*)(rec + R.elev);
     uint16_t* lpt = (uint16_t*)(rec + R.lptr);
     uint16_t* sch = (uint16_t*)(rec + R.sched);
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
             lm &= lm - 1;
             Lr[e] = Lf[i * ND + d];
             nbr[e] = (uint16_t)(i + doff<DIM>(d, ex, ey));
-            sgr[e] = (uint8_t)(t - lpt[v]);
+            rwr[e] = (uint16_t)i;
             pmap[i * ND + d] = e;
             ++e;
           }
@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       elv[depth] = (uint16_t)e;
       // backward entries: row i pulls L_ki z_k from its later neighbours k
       uint16_t* bk = (uint16_t*)(rec + R.bk);
-      uint16_t* bp = (uint16_t*)(rec + R.bp);
-      uint8_t* bsg = (uint8_t*)(rec + R.bsg);
+      double* bL = (double*)(rec + R.bL);
+      uint16_t* brw = (uint16_t*)(rec + R.brw);
       uint16_t* belv = (uint16_t*)(rec + R.belev);
       int f = 0;
       for (int v = 0; v < depth; ++v) {
@@ -275,8 +275,8 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
             um &= um - 1;
             const int k = i + doff<DIM>(d, ex, ey);
             bk[f] = (uint16_t)k;
-            bp[f] = (uint16_t)pmap[k * ND + (ND - 1 - d)];
-            bsg[f] = (uint8_t)(t - lpt[v]);
+            bL[f] = Lr[pmap[k * ND + (ND - 1 - d)]];
+            brw[f] = (uint16_t)i;
             ++f;
           }
         }

@@ -209,26 +209,55 @@ struct VcParams {
 // ballot), and the row's first lane subtracts the sum.  Rows of one level are
 // independent, so chunks need no synchronisation between them.  v is a 32-bit
 // offset into shared memory.
-__device__ __forceinline__ void seg_level(const double* __restrict__ L, const uint16_t* __restrict__ col,
-                                          const uint16_t* __restrict__ pos, const uint8_t* __restrict__ sg,
-                                          const uint16_t* __restrict__ sch, int eb, int ee, int rb, int v, int lane) {
-  for (int c0 = eb; c0 < ee; c0 += 32) {
-    const int q = c0 + lane;
-    const bool in = q < ee;
-    double val = 0.0;
-    int seg = -1;
-    if (in) { val = __ldg(L + (pos ? __ldg(pos + q) : q)) * vsm[v + __ldg(col + q)]; seg = __ldg(sg + q); }
-    const int ps = __shfl_up_sync(0xffffffffu, seg, 1);
-    const bool head = in && (lane == 0 || ps != seg);
-    const unsigned heads = __ballot_sync(0xffffffffu, head) | ~__ballot_sync(0xffffffffu, in);
-    // lanes (lane, lane+off] hold no row start  <=>  same row
-    const unsigned above = heads >> lane >> 1;
+__device__ __forceinline__ void seg_chunk(double lval, int colv, int row, bool in, int v, int lane) {
+  double val = in ? lval * vsm[v + colv] : 0.0;
+  const int key = in ? row : -1 - lane;
+  const int pk = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = in && (lane == 0 || pk != key);
+  const unsigned heads = __ballot_sync(0xffffffffu, head) | ~__ballot_sync(0xffffffffu, in);
+  // lanes (lane, lane+off] hold no row start  <=>  same row
+  const unsigned above = heads >> lane >> 1;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const double ov = __shfl_down_sync(0xffffffffu, val, off);
-      if ((above & ((1u << off) - 1u)) == 0u && lane + off < 32) val += ov;
+  for (int off = 1; off < 32; off <<= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, val, off);
+    if ((above & ((1u << off) - 1u)) == 0u && lane + off < 32) val += ov;
+  }
+  if (head) vsm[v + row] -= val;
+}
+
+// One triangular sweep, DAG level by level (levels reversed for the backward
+// sweep).  The first chunk of the next level is prefetched into registers while
+// the current level is reduced, so the global loads of the record overlap the
+// dependent shared-memory chain of the previous level.
+__device__ __forceinline__ void sweep_w(const double* __restrict__ Lv, const uint16_t* __restrict__ col,
+                                        const uint16_t* __restrict__ rw, const uint16_t* __restrict__ elv, int depth,
+                                        bool reverse, int v, int lane) {
+  int lv = reverse ? depth - 1 : 0;
+  int eb = __ldg(elv + lv), ee = __ldg(elv + lv + 1);
+  double pL = 0.0;
+  int pc = 0, pr = 0;
+  if (eb + lane < ee) { pL = __ldg(Lv + eb + lane); pc = __ldg(col + eb + lane); pr = __ldg(rw + eb + lane); }
+  for (int it = 0; it < depth; ++it) {
+    const int cb = eb, ce = ee;
+    const double cL = pL;
+    const int cc = pc, cr = pr;
+    const int nlv = reverse ? lv - 1 : lv + 1;
+    if (it + 1 < depth) {
+      eb = __ldg(elv + nlv);
+      ee = __ldg(elv + nlv + 1);
+      if (eb + lane < ee) { pL = __ldg(Lv + eb + lane); pc = __ldg(col + eb + lane); pr = __ldg(rw + eb + lane); }
     }
-    if (head) vsm[v + __ldg(sch + rb + seg)] -= val;
+    seg_chunk(cL, cc, cr, cb + lane < ce, v, lane);
+    for (int c0 = cb + 32; c0 < ce; c0 += 32) {
+      const int q = c0 + lane;
+      const bool in = q < ce;
+      double l2 = 0.0;
+      int c2 = 0, r2 = 0;
+      if (in) { l2 = __ldg(Lv + q); c2 = __ldg(col + q); r2 = __ldg(rw + q); }
+      seg_chunk(l2, c2, r2, in, v, lane);
+    }
+    __syncwarp();
+    lv = nlv;
   }
 }
 
@@ -239,26 +268,12 @@ __device__ __forceinline__ void ilu_w(const char* __restrict__ rec, bool act, in
   if (depth == 0) return;
   const RecLayout R = rec_layout(n, nL);
   const double* D = (const double*)(rec + R.D);
-  const double* L = (const double*)(rec + R.L);
-  const uint16_t* nb = (const uint16_t*)(rec + R.nb);
-  const uint8_t* sg = (const uint8_t*)(rec + R.sg);
-  const uint16_t* bk = (const uint16_t*)(rec + R.bk);
-  const uint16_t* bp = (const uint16_t*)(rec + R.bp);
-  const uint8_t* bsg = (const uint8_t*)(rec + R.bsg);
-  const uint16_t* elv = (const uint16_t*)(rec + R.elev);
-  const uint16_t* belv = (const uint16_t*)(rec + R.belev);
-  const uint16_t* lpt = (const uint16_t*)(rec + R.lptr);
-  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
-  for (int lv = 0; lv < depth; ++lv) {
-    seg_level(L, nb, nullptr, sg, sch, __ldg(elv + lv), __ldg(elv + lv + 1), __ldg(lpt + lv), v, lane);
-    __syncwarp();
-  }
+  sweep_w((const double*)(rec + R.L), (const uint16_t*)(rec + R.nb), (const uint16_t*)(rec + R.rw),
+          (const uint16_t*)(rec + R.elev), depth, false, v, lane);
   for (int i = lane; i < n; i += 32) vsm[v + i] = vsm[v + i] / __ldg(D + i);
   __syncwarp();
-  for (int lv = depth - 1; lv >= 0; --lv) {
-    seg_level(L, bk, bp, bsg, sch, __ldg(belv + lv), __ldg(belv + lv + 1), __ldg(lpt + lv), v, lane);
-    __syncwarp();
-  }
+  sweep_w((const double*)(rec + R.bL), (const uint16_t*)(rec + R.bk), (const uint16_t*)(rec + R.brw),
+          (const uint16_t*)(rec + R.belev), depth, true, v, lane);
 }
 
 // s = r - A_l z on the patch box (A_l row-major: ND contiguous doubles per node)
