@@ -119,6 +119,13 @@ struct lorpc_prec {
   double* Cd = nullptr;             // [J][ldc] dense coarse operators (column-major n_Ld x n_Ld)
   int ldc = 0;
   int lanes = 8;                    // lanes per patch in the V-cycle kernel
+  // thread-per-patch V-cycle (vcycle_t.cu): warp-interleaved factors, parking buffer
+  bool tmode = false;
+  char* trec = nullptr;
+  long long* trecoff = nullptr;
+  long long trec_bytes = 0;
+  double* zpark = nullptr;          // per-warp r_1 / z_1 scratch
+  double* Cdi = nullptr;            // dense coarse operators, interleaved by patch per warp
   // coarse space (R_0)
   int nc = 0;                       // GMG levels
   int cn[lorpc::MAXC][3];           // vertices per axis

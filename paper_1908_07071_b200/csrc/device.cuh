@@ -59,10 +59,15 @@ __device__ __forceinline__ double inv_det(const double* J, double* Ji) {
 }
 
 // 3^d stencil direction helpers: dir = (dx+1) + 3(dy+1) [+ 9(dz+1)]
+// LOR stencil matrices are stored node-major, NDP doubles per node (the ND
+// coefficients and a zero pad to a 16-byte multiple), so that one node's row is
+// contiguous and 16-byte aligned.
 template <int DIM> struct Dirs {
   static constexpr int ND = DIM == 2 ? 9 : 27;
+  static constexpr int NDP = DIM == 2 ? 10 : 28;
   static constexpr int CENTER = (ND - 1) / 2;
 };
+__host__ __device__ __forceinline__ int ndp_of(int dim) { return dim == 2 ? 10 : 28; }
 __host__ __device__ __forceinline__ int dir_dx(int d) { return d % 3 - 1; }
 __host__ __device__ __forceinline__ int dir_dy(int d) { return (d / 3) % 3 - 1; }
 __host__ __device__ __forceinline__ int dir_dz(int d) { return d / 9 - 1; }

@@ -99,7 +99,8 @@ __global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __re
     }
   }
 #pragma unroll
-  for (int d = 0; d < ND; ++d) A[g * ND + d] = row[d];
+  for (int d = 0; d < ND; ++d) A[g * Dirs<DIM>::NDP + d] = row[d];
+  A[g * Dirs<DIM>::NDP + ND] = 0.0;
 }
 
 // weight of coarse 1D index ic in the interpolation row of fine 1D index f
@@ -134,7 +135,7 @@ __global__ void k_galerkin(const double* __restrict__ Af, double* __restrict__ A
   const Axis1D* A3[3] = {&ax, &ay, &az};
   const long long Ncx = ax.Nc, Ncy = ay.Nc, Ncz = DIM == 3 ? az.Nc : 1;
   const long long Nfx = ax.Nf, Nfy = ay.Nf, Nfz = DIM == 3 ? az.Nf : 1;
-  const long long NcT = Ncx * Ncy * Ncz, NfT = Nfx * Nfy * Nfz;
+  const long long NcT = Ncx * Ncy * Ncz;
   const long long I = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (I >= NcT) return;
   const int Ic[3] = {(int)(I % Ncx), (int)((I / Ncx) % Ncy), (int)(I / (Ncx * Ncy))};
@@ -164,7 +165,7 @@ __global__ void k_galerkin(const double* __restrict__ Af, double* __restrict__ A
           const int b[3] = {fx + dir_dx(d), fy + dir_dy(d), fz + (DIM == 3 ? dir_dz(d) : 0)};
           if (b[0] < 0 || b[0] >= Nfx || b[1] < 0 || b[1] >= Nfy) continue;
           if (DIM == 3 && (b[2] < 0 || b[2] >= Nfz)) continue;
-          const double av = Af[a * ND + d];
+          const double av = Af[a * Dirs<DIM>::NDP + d];
           if (av == 0.0) continue;
           int c0[3], c1[3]; double w0[3], w1[3];
 #pragma unroll
@@ -195,7 +196,8 @@ __global__ void k_galerkin(const double* __restrict__ Af, double* __restrict__ A
     }
   }
 #pragma unroll
-  for (int d = 0; d < ND; ++d) Ac[I * ND + d] = row[d];
+  for (int d = 0; d < ND; ++d) Ac[I * Dirs<DIM>::NDP + d] = row[d];
+  Ac[I * Dirs<DIM>::NDP + ND] = 0.0;
 }
 
 static Transfer1D make_transfer(const double* xi, const std::vector<int>& fine, const std::vector<int>& coarse) {
@@ -248,7 +250,6 @@ int galerkin(int d, const double* Af, double* Ac, const Transfer1D& T, const int
 
 int lor_build(const lorpc_mesh* m, lorpc_lor* l, cudaStream_t s) {
   const int d = m->d;
-  const int ND = d == 2 ? 9 : 27;
   auto ch = make_chain(m->p);
   l->m = m;
   l->L = (int)ch.size();
@@ -261,7 +262,7 @@ int lor_build(const lorpc_mesh* m, lorpc_lor* l, cudaStream_t s) {
       l->Nax[lv][k] = (k < d) ? m->n[k] * (l->ml[lv] - 1) + 1 : 1;
       l->Nl[lv] *= l->Nax[lv][k];
     }
-    LORPC_TRY(dalloc(&l->A[lv], (size_t)ND * l->Nl[lv]));
+    LORPC_TRY(dalloc(&l->A[lv], (size_t)ndp_of(d) * l->Nl[lv]));
     if (lv + 1 < l->L) l->T[lv] = make_transfer(m->basis.xi, ch[lv], ch[lv + 1]);
   }
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);

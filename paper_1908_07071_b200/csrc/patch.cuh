@@ -72,29 +72,24 @@ __host__ __device__ __forceinline__ long long a8(long long b) { return (b + 7) &
 // once, in forward-solve order: grouped by DAG level of the triangular solve,
 // within a level by row (schedule order), within a row by direction:
 //   D[n]        pivots (natural index)
-//   L[nL]       L_ij of the forward sweep
-//   nb[nL]      column j (natural index, u16)
-//   rw[nL]      row i (natural index, u16): the segment key of the row reduction
-//   bL, bk, brw [nL]: the backward (L^T) entries, grouped the same way by DAG level
-//     and row i: value L_ki (duplicated so that no load depends on another), upper
-//     neighbour k, row i
-//   elev[n+1], belev[n+1]  entry offset of each DAG level (forward / backward)
-//   lptr[n+1], sched[n]    DAG level row pointers / rows in schedule order (setup)
+//   L[nL], nb[nL]   forward entries L_ij and columns j, rows in schedule order
+//   bL[nL], bk[nL]  backward (L^T) entries of row i: L_ki (value duplicated, so no
+//                   load depends on another) and the later neighbour k
+//   frp[n+1], brp[n+1]  entry offsets of the row sched[t] (forward / backward)
+//   lptr[n+1]   DAG level row pointers into sched;  sched[n] rows (natural index)
 //   order[n]    elimination order (export only)
-// Both sweeps pull, with a segmented warp reduction per row (deterministic).
-struct RecLayout { long long D, L, nb, rw, bL, bk, brw, elev, belev, lptr, sched, order, total; };
+// Each lane sweeps whole rows (row-per-lane, rows of one DAG level in parallel).
+struct RecLayout { long long D, L, nb, bL, bk, frp, brp, lptr, sched, order, total; };
 __host__ __device__ __forceinline__ RecLayout rec_layout(int n, long long nL) {
   RecLayout R;
   R.D = 16;
   R.L = R.D + 8ll * n;
   R.nb = R.L + 8ll * nL;
-  R.rw = R.nb + a8(2ll * nL);
-  R.bL = R.rw + a8(2ll * nL);
+  R.bL = R.nb + a8(2ll * nL);
   R.bk = R.bL + 8ll * nL;
-  R.brw = R.bk + a8(2ll * nL);
-  R.elev = R.brw + a8(2ll * nL);
-  R.belev = R.elev + a8(2ll * (n + 1));
-  R.lptr = R.belev + a8(2ll * (n + 1));
+  R.frp = R.bk + a8(2ll * nL);
+  R.brp = R.frp + a8(2ll * (n + 1));
+  R.lptr = R.brp + a8(2ll * (n + 1));
   R.sched = R.lptr + a8(2ll * (n + 1));
   R.order = R.sched + a8(2ll * n);
   R.total = (R.order + 2ll * n + 15) & ~15ll;  // 16-byte aligned patch records
@@ -132,7 +127,7 @@ __device__ __forceinline__ double stencil_apply(const double* A, const double* z
   double acc = 0.0;
   for (int d = 0; d < ND; ++d) {
     const long long o = dir_dx(d) + (long long)Nv.x * (dir_dy(d) + (long long)Nv.y * (DIM == 3 ? dir_dz(d) : 0));
-    acc += A[g * ND + d] * z[g + o];
+    acc += A[g * Dirs<DIM>::NDP + d] * z[g + o];
   }
   return acc;
 }

@@ -29,6 +29,8 @@ int galerkin(int d, const double* Af, double* Ac, const Transfer1D& T, const int
              cudaStream_t s);
 Transfer1D gmg_transfer();
 int dense_coarse_setup(lorpc_prec* b, cudaStream_t s);  // vcycle.cu
+int trec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_t.cu
+size_t tmode_smem(const lorpc_prec* b);
 
 // ------------------------------------------------------------------ MDF + ILU(0)
 __device__ __forceinline__ double q30(double x) {
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       const long long gi = (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0));
       const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
       for (int d = 0; d < ND; ++d) {
-        At[i * ND + d] = ((em >> d) & 1u) ? A[gi * ND + d] : 0.0;
+        At[i * ND + d] = ((em >> d) & 1u) ? A[gi * Dirs<DIM>::NDP + d] : 0.0;
         Lf[i * ND + d] = 0.0;
       }
       alive[i] = 1;
@@ -199,8 +201,7 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
     double* Dr = (double*)(rec + R.D);
     double* Lr = (double*)(rec + R.L);
     uint16_t* nbr = (uint16_t*)(rec + R.nb);
-    uint16_t* rwr = (uint16_t*)(rec + R.rw);
-    uint16_t* elv = (uint16_t*)(rec + R.elev);
+    uint16_t* frp = (uint16_t*)(rec + R.frp);
     uint16_t* lpt = (uint16_t*)(rec + R.lptr);
     uint16_t* sch = (uint16_t*)(rec + R.sched);
     uint16_t* orr = (uint16_t*)(rec + R.order);
@@ -239,49 +240,42 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       for (int v = 0; v < depth; ++v) { lpt[v] = (uint16_t)acc; const int c = cnt[v]; cnt[v] = acc; acc += c; }
       lpt[depth] = (uint16_t)acc;
       for (int t = 0; t < n; ++t) { const int i = ord[t]; sch[cnt[lev[i]]++] = (uint16_t)i; }
-      // entries grouped by level, then row, then direction
+      // forward entries: rows in schedule order, each row's lower neighbours by direction
       int e = 0;
-      for (int v = 0; v < depth; ++v) {
-        elv[v] = (uint16_t)e;
-        for (int t = lpt[v]; t < lpt[v + 1]; ++t) {
-          const int i = sch[t];
-          uint32_t lm = (uint32_t)lmk[i];
-          while (lm) {
-            const int d = __ffs(lm) - 1;
-            lm &= lm - 1;
-            Lr[e] = Lf[i * ND + d];
-            nbr[e] = (uint16_t)(i + doff<DIM>(d, ex, ey));
-            rwr[e] = (uint16_t)i;
-            pmap[i * ND + d] = e;
-            ++e;
-          }
+      for (int t = 0; t < n; ++t) {
+        const int i = sch[t];
+        frp[t] = (uint16_t)e;
+        uint32_t lm = (uint32_t)lmk[i];
+        while (lm) {
+          const int d = __ffs(lm) - 1;
+          lm &= lm - 1;
+          Lr[e] = Lf[i * ND + d];
+          nbr[e] = (uint16_t)(i + doff<DIM>(d, ex, ey));
+          pmap[i * ND + d] = e;
+          ++e;
         }
       }
-      elv[depth] = (uint16_t)e;
+      frp[n] = (uint16_t)e;
       // backward entries: row i pulls L_ki z_k from its later neighbours k
       uint16_t* bk = (uint16_t*)(rec + R.bk);
       double* bL = (double*)(rec + R.bL);
-      uint16_t* brw = (uint16_t*)(rec + R.brw);
-      uint16_t* belv = (uint16_t*)(rec + R.belev);
+      uint16_t* brp = (uint16_t*)(rec + R.brp);
       int f = 0;
-      for (int v = 0; v < depth; ++v) {
-        belv[v] = (uint16_t)f;
-        for (int t = lpt[v]; t < lpt[v + 1]; ++t) {
-          const int i = sch[t];
-          const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
-          uint32_t um = exist_mask<DIM>(ix, iy, iz, ex, ey, ez) & ~(uint32_t)lmk[i] & ~(1u << C);
-          while (um) {
-            const int d = __ffs(um) - 1;
-            um &= um - 1;
-            const int k = i + doff<DIM>(d, ex, ey);
-            bk[f] = (uint16_t)k;
-            bL[f] = Lr[pmap[k * ND + (ND - 1 - d)]];
-            brw[f] = (uint16_t)i;
-            ++f;
-          }
+      for (int t = 0; t < n; ++t) {
+        const int i = sch[t];
+        brp[t] = (uint16_t)f;
+        const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
+        uint32_t um = exist_mask<DIM>(ix, iy, iz, ex, ey, ez) & ~(uint32_t)lmk[i] & ~(1u << C);
+        while (um) {
+          const int d = __ffs(um) - 1;
+          um &= um - 1;
+          const int k = i + doff<DIM>(d, ex, ey);
+          bk[f] = (uint16_t)k;
+          bL[f] = Lr[pmap[k * ND + (ND - 1 - d)]];
+          ++f;
         }
       }
-      belv[depth] = (uint16_t)f;
+      brp[n] = (uint16_t)f;
       int* h = (int*)rec;
       h[0] = n; h[1] = depth; h[2] = (int)nL; h[3] = l;
     }
@@ -303,7 +297,7 @@ __global__ void k_l1diag(const double* __restrict__ A, double* __restrict__ dl, 
     const int o[3] = {dir_dx(d), dir_dy(d), dir_dz(d)};
     bool in = true;
     for (int k = 0; k < DIM; ++k) { const int v = c[k] + o[k]; if (v <= 0 || v >= Nn[k] - 1) in = false; }
-    if (in) s += fabs(A[g * ND + d]);
+    if (in) s += fabs(A[g * Dirs<DIM>::NDP + d]);
   }
   dl[g] = s;
 }
@@ -328,7 +322,7 @@ __global__ void k_coarsest_factor(const double* __restrict__ A, double* __restri
       // interior rank of h
       int rk = 0;
       for (long long t = 0; t < h; ++t) { int c2[3]; if (interior_of<DIM>(t, Nv, c2)) ++rk; }
-      F[idx * nint + rk] = A[g * ND + d];
+      F[idx * nint + rk] = A[g * Dirs<DIM>::NDP + d];
     }
     ++idx;
   }
@@ -492,7 +486,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
       int nxt[3] = {cur[0], cur[1], cur[2]};
       for (int k = 0; k < d; ++k) nxt[k] = (cur[k] - 1) / 2 + 1;
       long long Nn = (long long)nxt[0] * nxt[1] * nxt[2];
-      LORPC_TRY(dalloc(&b->Ac[lvl + 1], (size_t)ND * Nn));
+      LORPC_TRY(dalloc(&b->Ac[lvl + 1], (size_t)ndp_of(d) * Nn));
       int ne[3] = {nxt[0] - 1, nxt[1] - 1, nxt[2] - 1};
       LORPC_TRY(galerkin(d, b->Ac[lvl], b->Ac[lvl + 1], gmg_transfer(), ne, cur, nxt, s));
       for (int k = 0; k < 3; ++k) cur[k] = nxt[k];
@@ -521,6 +515,10 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   LORPC_TRY(dalloc(&b->Cd, (size_t)b->J * b->ldc));
   LORPC_TRY(dense_coarse_setup(b, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
+  // thread-per-patch V-cycle when the warp's 32 patch vectors fit in shared memory
+  b->tmode = b->Ld == 1 && b->max_n[1] <= 32 && tmode_smem(b) <= 227 * 1024 && 33ll * (b->max_n[0] + 1) < 65536;
+  if (const char* e = getenv("LORPC_TMODE")) b->tmode = b->tmode && atoi(e) != 0;
+  if (b->tmode) LORPC_TRY(trec_build(b, s));
   return LORPC_OK;
 }
 

@@ -174,14 +174,16 @@ __global__ void k_coarsest_solve(const double* __restrict__ F, const double* __r
 
 
 // ------------------------------------------------------------------ patch V-cycle
-// One warp per patch (G = 32 lanes).  Shared memory per patch: the level vectors
-// [r_l | z_l | s_l] for the finest levels, [r | z] at the dense level Ld, and a
-// transfer scratch, all addressed by 32-bit offsets into the dynamic array.
-// The ILU records are read with __ldg; the level operators A_l row-major.
+// VG = 8 lanes per patch, 4 patches per warp.  Shared memory per patch: the level
+// vectors [r_l | z_l | s_l] for the finest levels, [r | z] at the dense level Ld,
+// and a transfer scratch, addressed by 32-bit offsets into the dynamic array.
+// ILU sweeps are row-per-lane: the rows of one DAG level (3-6 per patch on the
+// MDF-ordered 3D patches) go to the lanes of the patch's group, each lane walks
+// its row's entries; the next level's row data is prefetched into registers.
 // Levels >= Ld (<= 32 free nodes per patch) are replaced by one precomputed dense
-// symmetric matrix per patch: the exact operator of the V-cycle restricted to
-// those levels (built by k_dense_coarse from the same ILU records), so the whole
-// coarse part of the cycle is one matrix-vector product.
+// symmetric matrix per patch, the exact operator of the V-cycle on those levels
+// (k_dense_coarse builds it from the same ILU records).
+constexpr int VG = 8, VPPW = 32 / VG;
 extern __shared__ __align__(16) double vsm[];
 
 struct VcParams {
@@ -203,91 +205,80 @@ struct VcParams {
   double* z;
 };
 
-// One DAG level of a triangular sweep: the level's entries [eb, ee) are contiguous;
-// each lane multiplies one entry, a segmented shuffle reduction sums each row's
-// entries (rows contiguous in the level; the row starts of a chunk come from one
-// ballot), and the row's first lane subtracts the sum.  Rows of one level are
-// independent, so chunks need no synchronisation between them.  v is a 32-bit
-// offset into shared memory.
-__device__ __forceinline__ void seg_chunk(double lval, int colv, int row, bool in, int v, int lane) {
-  double val = in ? lval * vsm[v + colv] : 0.0;
-  const int key = in ? row : -1 - lane;
-  const int pk = __shfl_up_sync(0xffffffffu, key, 1);
-  const bool head = in && (lane == 0 || pk != key);
-  const unsigned heads = __ballot_sync(0xffffffffu, head) | ~__ballot_sync(0xffffffffu, in);
-  // lanes (lane, lane+off] hold no row start  <=>  same row
-  const unsigned above = heads >> lane >> 1;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const double ov = __shfl_down_sync(0xffffffffu, val, off);
-    if ((above & ((1u << off) - 1u)) == 0u && lane + off < 32) val += ov;
-  }
-  if (head) vsm[v + row] -= val;
-}
-
-// One triangular sweep, DAG level by level (levels reversed for the backward
-// sweep).  The first chunk of the next level is prefetched into registers while
-// the current level is reduced, so the global loads of the record overlap the
-// dependent shared-memory chain of the previous level.
-__device__ __forceinline__ void sweep_w(const double* __restrict__ Lv, const uint16_t* __restrict__ col,
-                                        const uint16_t* __restrict__ rw, const uint16_t* __restrict__ elv, int depth,
-                                        bool reverse, int v, int lane) {
-  int lv = reverse ? depth - 1 : 0;
-  int eb = __ldg(elv + lv), ee = __ldg(elv + lv + 1);
-  double pL = 0.0;
-  int pc = 0, pr = 0;
-  if (eb + lane < ee) { pL = __ldg(Lv + eb + lane); pc = __ldg(col + eb + lane); pr = __ldg(rw + eb + lane); }
-  for (int it = 0; it < depth; ++it) {
-    const int cb = eb, ce = ee;
-    const double cL = pL;
-    const int cc = pc, cr = pr;
-    const int nlv = reverse ? lv - 1 : lv + 1;
-    if (it + 1 < depth) {
-      eb = __ldg(elv + nlv);
-      ee = __ldg(elv + nlv + 1);
-      if (eb + lane < ee) { pL = __ldg(Lv + eb + lane); pc = __ldg(col + eb + lane); pr = __ldg(rw + eb + lane); }
-    }
-    seg_chunk(cL, cc, cr, cb + lane < ce, v, lane);
-    for (int c0 = cb + 32; c0 < ce; c0 += 32) {
-      const int q = c0 + lane;
-      const bool in = q < ce;
-      double l2 = 0.0;
-      int c2 = 0, r2 = 0;
-      if (in) { l2 = __ldg(Lv + q); c2 = __ldg(col + q); r2 = __ldg(rw + q); }
-      seg_chunk(l2, c2, r2, in, v, lane);
+// One triangular sweep of one patch level, DAG level by DAG level (reversed for
+// the backward sweep): lane gl of the group takes rows lptr[lv] + gl, + VG, ...
+// md = warp-uniform number of levels (max over the warp's patches).
+__device__ __forceinline__ void sweep_rows(const double* __restrict__ Lv, const uint16_t* __restrict__ col,
+                                           const uint16_t* __restrict__ rp, const uint16_t* __restrict__ sch,
+                                           const uint16_t* __restrict__ lpt, int depth, int md, bool reverse, int v,
+                                           int gl) {
+  // prefetched row of the next level: node, entry range
+  int prow = -1, pe0 = 0, pe1 = 0, pt = 0, pt1 = 0;
+  auto fetch = [&](int it) {
+    prow = -1;
+    if (it >= depth) return;
+    const int lv = reverse ? depth - 1 - it : it;
+    pt = __ldg(lpt + lv) + gl;
+    pt1 = __ldg(lpt + lv + 1);
+    if (pt < pt1) { prow = __ldg(sch + pt); pe0 = __ldg(rp + pt); pe1 = __ldg(rp + pt + 1); }
+  };
+  fetch(0);
+  for (int it = 0; it < md; ++it) {
+    int row = prow, e0 = pe0, e1 = pe1, t = pt;
+    const int t1 = pt1;
+    fetch(it + 1);
+    while (row >= 0) {
+      double a0 = vsm[v + row], a1 = 0.0;
+      int e = e0;
+      for (; e + 3 < e1; e += 4) {
+        const double l0 = __ldg(Lv + e), l1 = __ldg(Lv + e + 1), l2 = __ldg(Lv + e + 2), l3 = __ldg(Lv + e + 3);
+        const int c0 = __ldg(col + e), c1 = __ldg(col + e + 1), c2 = __ldg(col + e + 2), c3 = __ldg(col + e + 3);
+        a0 -= l0 * vsm[v + c0];
+        a1 -= l1 * vsm[v + c1];
+        a0 -= l2 * vsm[v + c2];
+        a1 -= l3 * vsm[v + c3];
+      }
+      for (; e < e1; ++e) a0 -= __ldg(Lv + e) * vsm[v + __ldg(col + e)];
+      vsm[v + row] = a0 + a1;
+      // a level wider than VG rows: further rows of this lane
+      t += VG;
+      row = -1;
+      if (t < t1) { row = __ldg(sch + t); e0 = __ldg(rp + t); e1 = __ldg(rp + t + 1); }
     }
     __syncwarp();
-    lv = nlv;
   }
 }
 
 // v := M^{-1} v, M = L D L^T of one patch level (forward L, diagonal, backward L^T)
-__device__ __forceinline__ void ilu_w(const char* __restrict__ rec, bool act, int v, int lane) {
+__device__ __forceinline__ void ilu_w(const char* __restrict__ rec, bool act, int v, int gl) {
   int n = 0, depth = 0, nL = 0;
   if (act) { const int4 h = __ldg((const int4*)rec); n = h.x; depth = h.y; nL = h.z; }
-  if (depth == 0) return;
+  const int md = __reduce_max_sync(0xffffffffu, depth);
+  if (md == 0) return;
   const RecLayout R = rec_layout(n, nL);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* lpt = (const uint16_t*)(rec + R.lptr);
+  sweep_rows((const double*)(rec + R.L), (const uint16_t*)(rec + R.nb), (const uint16_t*)(rec + R.frp), sch, lpt,
+             depth, md, false, v, gl);
   const double* D = (const double*)(rec + R.D);
-  sweep_w((const double*)(rec + R.L), (const uint16_t*)(rec + R.nb), (const uint16_t*)(rec + R.rw),
-          (const uint16_t*)(rec + R.elev), depth, false, v, lane);
-  for (int i = lane; i < n; i += 32) vsm[v + i] = vsm[v + i] / __ldg(D + i);
+  for (int i = gl; i < n; i += VG) vsm[v + i] = vsm[v + i] / __ldg(D + i);
   __syncwarp();
-  sweep_w((const double*)(rec + R.bL), (const uint16_t*)(rec + R.bk), (const uint16_t*)(rec + R.brw),
-          (const uint16_t*)(rec + R.belev), depth, true, v, lane);
+  sweep_rows((const double*)(rec + R.bL), (const uint16_t*)(rec + R.bk), (const uint16_t*)(rec + R.brp), sch, lpt,
+             depth, md, true, v, gl);
 }
 
 // s = r - A_l z on the patch box (A_l row-major: ND contiguous doubles per node)
 template <int DIM>
-__device__ __forceinline__ void residual_w(const double* __restrict__ A, long long Nx, long long Ny, const int* lo,
-                                           const int* ext, int r, int z, int s, int lane) {
+__device__ __forceinline__ void residual_w(const double* __restrict__ A, long long Nx, long long Ny, long long NT, const int* lo,
+                                           const int* ext, int r, int z, int s, int gl) {
   constexpr int ND = Dirs<DIM>::ND;
   const int ex = ext[0], ey = ext[1], ez = ext[2], n = ex * ey * ez;
   const float rex = 1.0f / ex, rexy = 1.0f / (ex * ey);
-  for (int i = lane; i < n; i += 32) {
+  for (int i = gl; i < n; i += VG) {
     int ix, iy, iz;
     box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
     const long long gi = (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0));
-    const double* Ar = A + gi * ND;
+    const double* Ar = A + gi * Dirs<DIM>::NDP;
     const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
     double a0 = vsm[r + i], a1 = 0.0;
 #pragma unroll
@@ -303,18 +294,18 @@ __device__ __forceinline__ void residual_w(const double* __restrict__ A, long lo
 // rc = P^T s (separable: x, y, z passes through the scratch T at offset t)
 template <int DIM>
 __device__ __forceinline__ void restrict_w(const double* Wx, const double* Wy, const double* Wz, const int* ext,
-                                           const int* cext, int s, int rc, int t, int lane) {
+                                           const int* cext, int s, int rc, int t, int gl) {
   const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
-  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy);
+  const float rcx = 1.0f / max(cx, 1), rcxy = 1.0f / max(cx * cy, 1);
   const int T2 = DIM == 3 ? t + cx * fy * fz : rc;
-  for (int u = lane; u < cx * fy * fz; u += 32) {
+  for (int u = gl; u < cx * fy * fz; u += VG) {
     const int rest = qdiv(u, rcx), ic = u - rest * cx;
     double a = 0.0;
     for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * vsm[s + f + fx * rest];
     vsm[t + u] = a;
   }
   __syncwarp();
-  for (int u = lane; u < cx * cy * fz; u += 32) {
+  for (int u = gl; u < cx * cy * fz; u += VG) {
     const int kf = qdiv(u, rcxy), r2 = u - kf * cx * cy, jc = qdiv(r2, rcx), ic = r2 - jc * cx;
     double a = 0.0;
     for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * vsm[t + ic + cx * (f + fy * kf)];
@@ -322,7 +313,7 @@ __device__ __forceinline__ void restrict_w(const double* Wx, const double* Wy, c
   }
   __syncwarp();
   if (DIM == 3) {
-    for (int u = lane; u < cx * cy * cz; u += 32) {
+    for (int u = gl; u < cx * cy * cz; u += VG) {
       const int kc = qdiv(u, rcxy), ij = u - kc * cx * cy;
       double a = 0.0;
       for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * vsm[T2 + ij + cx * cy * f];
@@ -335,13 +326,14 @@ __device__ __forceinline__ void restrict_w(const double* Wx, const double* Wy, c
 // z += P e (separable transpose of restrict_w)
 template <int DIM>
 __device__ __forceinline__ void prolong_w(const double* Wx, const double* Wy, const double* Wz, const int* ext,
-                                          const int* cext, int e, int z, int t, int lane) {
+                                          const int* cext, int e, int z, int t, int gl) {
   const int fx = ext[0], fy = ext[1], fz = ext[2], cx = cext[0], cy = cext[1], cz = cext[2];
-  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
+  const float rcx = 1.0f / max(cx, 1), rcxy = 1.0f / max(cx * cy, 1), rcxfy = 1.0f / max(cx * fy, 1),
+              rfx = 1.0f / max(fx, 1);
   int U2 = e;
   if (DIM == 3) {
     U2 = t + cx * fy * fz;
-    for (int u = lane; u < cx * cy * fz; u += 32) {          // z pass: [cx][cy][fz]
+    for (int u = gl; u < cx * cy * fz; u += VG) {           // z pass: [cx][cy][fz]
       const int kf = qdiv(u, rcxy), ij = u - kf * cx * cy;
       double a = 0.0;
       for (int c = 0; c < cz; ++c) a += __ldg(Wz + c * fz + kf) * vsm[e + ij + cx * cy * c];
@@ -349,7 +341,7 @@ __device__ __forceinline__ void prolong_w(const double* Wx, const double* Wy, co
     }
     __syncwarp();
   }
-  for (int u = lane; u < cx * fy * fz; u += 32) {            // y pass: [cx][fy][fz]
+  for (int u = gl; u < cx * fy * fz; u += VG) {             // y pass: [cx][fy][fz]
     const int kf = qdiv(u, rcxfy), r2 = u - kf * cx * fy, jf = qdiv(r2, rcx), ic = r2 - jf * cx;
     double a = 0.0;
     for (int c = 0; c < cy; ++c) a += __ldg(Wy + c * fy + jf) * vsm[U2 + ic + cx * (c + cy * kf)];
@@ -357,7 +349,7 @@ __device__ __forceinline__ void prolong_w(const double* Wx, const double* Wy, co
   }
   __syncwarp();
   const int n = fx * fy * fz;
-  for (int i = lane; i < n; i += 32) {                        // x pass, z += P e
+  for (int i = gl; i < n; i += VG) {                         // x pass, z += P e
     const int rest = qdiv(i, rfx), fxi = i - rest * fx;
     double a = 0.0;
     for (int c = 0; c < cx; ++c) a += __ldg(Wx + c * fx + fxi) * vsm[t + c + cx * rest];
@@ -366,7 +358,7 @@ __device__ __forceinline__ void prolong_w(const double* Wx, const double* Wy, co
   __syncwarp();
 }
 
-// Patch geometry of one warp's patch
+// Patch geometry of one group's patch
 struct PatchCtx {
   int elo[3], ec[3];
   bool act;
@@ -387,7 +379,7 @@ __device__ __forceinline__ void box_of(const VcParams& P, const PatchCtx& c, int
 // Input r_{l0} at soff[l0], output z_{l0} at soff[l0] + nmax[l0].
 template <int DIM>
 __device__ void vcycle_range(const VcParams& P, const PatchCtx& c, long long j, int base, int l0, int l1, bool dense,
-                             int lane) {
+                             int gl) {
   const int L = P.G.L;
   auto rv = [&](int l) { return base + P.soff[l]; };
   auto zv = [&](int l) { return base + P.soff[l] + P.nmax[l]; };
@@ -399,21 +391,21 @@ __device__ void vcycle_range(const VcParams& P, const PatchCtx& c, long long j, 
     box_of<DIM>(P, c, l, lo, ext);
     box_of<DIM>(P, c, l + 1, clo, cext);
     const int n = ext[0] * ext[1] * ext[2];
-    for (int i = lane; i < n; i += 32) vsm[zv(l) + i] = vsm[rv(l) + i];
+    for (int i = gl; i < n; i += VG) vsm[zv(l) + i] = vsm[rv(l) + i];
     __syncwarp();
-    ilu_w(recl(l), c.act, zv(l), lane);                       // pre-smoothing
-    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, rv(l), zv(l), sv(l), lane);
+    ilu_w(recl(l), c.act, zv(l), gl);                          // pre-smoothing
+    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], (long long)P.G.Nax[l][0] * P.G.Nax[l][1] * P.G.Nax[l][2], lo, ext, rv(l), zv(l), sv(l), gl);
     __syncwarp();
     restrict_w<DIM>(P.W + P.woff[l][c.ec[0]], P.W + P.woff[l][c.ec[1]], P.W + P.woff[l][DIM == 3 ? c.ec[2] : 1],
-                    ext, cext, sv(l), rv(l + 1), T, lane);
+                    ext, cext, sv(l), rv(l + 1), T, gl);
   }
   {
     int lo[3], ext[3];
     box_of<DIM>(P, c, l1, lo, ext);
     const int n = ext[0] * ext[1] * ext[2];
-    if (dense) {                                              // z = C r (column-major, symmetric)
+    if (dense) {                                               // z = C r (column-major, symmetric)
       const double* C = P.Cd + (c.act ? j : 0) * (long long)P.ldc;
-      for (int i = lane; i < n; i += 32) {
+      for (int i = gl; i < n; i += VG) {
         double a0 = 0.0, a1 = 0.0;
         int k = 0;
         for (; k + 1 < n; k += 2) {
@@ -425,9 +417,9 @@ __device__ void vcycle_range(const VcParams& P, const PatchCtx& c, long long j, 
       }
       __syncwarp();
     } else {
-      for (int i = lane; i < n; i += 32) vsm[zv(l1) + i] = vsm[rv(l1) + i];
+      for (int i = gl; i < n; i += VG) vsm[zv(l1) + i] = vsm[rv(l1) + i];
       __syncwarp();
-      ilu_w(recl(l1), c.act, zv(l1), lane);
+      ilu_w(recl(l1), c.act, zv(l1), gl);
     }
   }
   for (int l = l1 - 1; l >= l0; --l) {
@@ -436,11 +428,11 @@ __device__ void vcycle_range(const VcParams& P, const PatchCtx& c, long long j, 
     box_of<DIM>(P, c, l + 1, clo, cext);
     const int n = ext[0] * ext[1] * ext[2];
     prolong_w<DIM>(P.W + P.woff[l][c.ec[0]], P.W + P.woff[l][c.ec[1]], P.W + P.woff[l][DIM == 3 ? c.ec[2] : 1],
-                   ext, cext, zv(l + 1), zv(l), T, lane);
-    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], lo, ext, rv(l), zv(l), sv(l), lane);
+                   ext, cext, zv(l + 1), zv(l), T, gl);
+    residual_w<DIM>(P.A[l], P.G.Nax[l][0], P.G.Nax[l][1], (long long)P.G.Nax[l][0] * P.G.Nax[l][1] * P.G.Nax[l][2], lo, ext, rv(l), zv(l), sv(l), gl);
     __syncwarp();
-    ilu_w(recl(l), c.act, sv(l), lane);                       // post-smoothing
-    for (int i = lane; i < n; i += 32) vsm[zv(l) + i] += vsm[sv(l) + i];
+    ilu_w(recl(l), c.act, sv(l), gl);                          // post-smoothing
+    for (int i = gl; i < n; i += VG) vsm[zv(l) + i] += vsm[sv(l) + i];
     __syncwarp();
   }
 }
@@ -459,25 +451,26 @@ __device__ __forceinline__ PatchCtx patch_ctx(const VcParams& P, long long j) {
 
 template <int DIM>
 __global__ void __launch_bounds__(128, LORPC_VC_MINB) k_vcycle(VcParams P) {
-  const int lane = threadIdx.x & 31;
-  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (j >= P.J) return;  // warp-uniform
-  const int base = (threadIdx.x >> 5) * P.patch_doubles;
+  const int lane = threadIdx.x & 31, grp = lane / VG, gl = lane % VG;
+  const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (wg * VPPW >= P.J) return;  // warp-uniform
+  const long long j = wg * VPPW + grp;
+  const int base = ((threadIdx.x >> 5) * VPPW + grp) * P.patch_doubles;
   const PatchCtx c = patch_ctx<DIM>(P, j);
   int lo[3], ext[3];
   box_of<DIM>(P, c, 0, lo, ext);
   const int n = ext[0] * ext[1] * ext[2];
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-  const float rex = 1.0f / ext[0], rexy = 1.0f / (ext[0] * ext[1]);
-  for (int i = lane; i < n; i += 32) {                        // r_j = I_j^T r (a5)
+  const float rex = 1.0f / max(ext[0], 1), rexy = 1.0f / max(ext[0] * ext[1], 1);
+  for (int i = gl; i < n; i += VG) {                          // r_j = I_j^T r (a5)
     int ix, iy, iz;
     box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
     vsm[base + P.soff[0] + i] = __ldg(P.r + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)));
   }
   __syncwarp();
-  vcycle_range<DIM>(P, c, j, base, 0, P.Ld, true, lane);
+  vcycle_range<DIM>(P, c, j, base, 0, P.Ld, true, gl);
   const int z0 = base + P.soff[0] + P.nmax[0];
-  for (int i = lane; i < n; i += 32) {                        // z += I_j z_j (a8)
+  for (int i = gl; i < n; i += VG) {                          // z += I_j z_j (a8)
     int ix, iy, iz;
     box_xyz(i, ext[0], ext[1], rex, rexy, ix, iy, iz);
     atomicAdd(P.z + (lo[0] + ix) + Nx * ((lo[1] + iy) + Ny * (DIM == 3 ? lo[2] + iz : 0)), vsm[z0 + i]);
@@ -485,24 +478,29 @@ __global__ void __launch_bounds__(128, LORPC_VC_MINB) k_vcycle(VcParams P) {
 }
 
 // setup: dense operator of the V-cycle on levels Ld..L-1 for every patch (columns
-// = images of the unit vectors), one warp per patch
+// = images of the unit vectors); warp-uniform column loop
 template <int DIM>
 __global__ void __launch_bounds__(128) k_dense_coarse(VcParams P) {
-  const int lane = threadIdx.x & 31;
-  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  if (j >= P.J) return;
-  const int base = (threadIdx.x >> 5) * P.patch_doubles;
-  const PatchCtx c = patch_ctx<DIM>(P, j);
+  const int lane = threadIdx.x & 31, grp = lane / VG, gl = lane % VG;
+  const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (wg * VPPW >= P.J) return;
+  const long long j = wg * VPPW + grp;
+  const int base = ((threadIdx.x >> 5) * VPPW + grp) * P.patch_doubles;
+  PatchCtx c = patch_ctx<DIM>(P, j);
   const int Ld = P.Ld, L = P.G.L;
   int lo[3], ext[3];
   box_of<DIM>(P, c, Ld, lo, ext);
   const int n = ext[0] * ext[1] * ext[2];
-  double* C = P.Cd + j * (long long)P.ldc;
-  for (int k = 0; k < n; ++k) {
-    for (int i = lane; i < n; i += 32) vsm[base + P.soff[Ld] + i] = (i == k) ? 1.0 : 0.0;
+  const int nw = __reduce_max_sync(0xffffffffu, n);
+  double* C = P.Cd + (c.act ? j : 0) * (long long)P.ldc;
+  const bool act0 = c.act;
+  for (int k = 0; k < nw; ++k) {
+    c.act = act0 && k < n;
+    for (int i = gl; i < n; i += VG) vsm[base + P.soff[Ld] + i] = (i == k) ? 1.0 : 0.0;
     __syncwarp();
-    vcycle_range<DIM>(P, c, j, base, Ld, L - 1, false, lane);
-    for (int i = lane; i < n; i += 32) C[(long long)k * n + i] = vsm[base + P.soff[Ld] + P.nmax[Ld] + i];
+    vcycle_range<DIM>(P, c, j, base, Ld, L - 1, false, gl);
+    if (c.act)
+      for (int i = gl; i < n; i += VG) C[(long long)k * n + i] = vsm[base + P.soff[Ld] + P.nmax[Ld] + i];
     __syncwarp();
   }
 }
@@ -578,11 +576,13 @@ static VcParams make_params(const lorpc_prec* b, const double* r, double* z) {
 
 template <int DIM, bool SETUP>
 static int launch_vc(const VcParams& P, long long J, cudaStream_t s) {
-  const size_t per_warp = (size_t)P.patch_doubles * sizeof(double);
-  const int wpb = 4;
+  const size_t per_warp = (size_t)VPPW * P.patch_doubles * sizeof(double);
+  int wpb = 4;
+  while (wpb > 1 && per_warp * wpb > 113 * 1024) wpb >>= 1;
   const size_t smem = per_warp * wpb;
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle: patch does not fit in shared memory");
-  const unsigned blocks = (unsigned)((J + wpb - 1) / wpb);
+  const long long warps = (J + VPPW - 1) / VPPW;
+  const unsigned blocks = (unsigned)((warps + wpb - 1) / wpb);
   if (SETUP) {
     cudaFuncSetAttribute(k_dense_coarse<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_dense_coarse<DIM><<<blocks, 32 * wpb, smem, s>>>(P);
@@ -593,6 +593,8 @@ static int launch_vc(const VcParams& P, long long J, cudaStream_t s) {
   LORPC_LAUNCHED();
   return LORPC_OK;
 }
+
+int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);  // vcycle_t.cu
 
 int dense_coarse_setup(lorpc_prec* b, cudaStream_t s) {
   VcParams P = make_params(b, nullptr, nullptr);
@@ -607,7 +609,8 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   lorpc_prec* bm = const_cast<lorpc_prec*>(b);
   const bool prof = bm->prof_on && bm->prof_n < (int)bm->prof_ev.size() / 2;
   if (prof) LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n], s));
-  const int rc = d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
+  const int rc = b->tmode ? vcycle_t_apply(b, r, z, s)
+                 : d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
   if (rc != LORPC_OK) return rc;
   if (prof) { LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n + 1], s)); bm->prof_n++; }
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
