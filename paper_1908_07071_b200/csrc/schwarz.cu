@@ -116,7 +116,6 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
       continue;
     }
     const long long Nx = P.G.Nax[l][0], Ny = P.G.Nax[l][1];
-    const long long NT = Nx * Ny * P.G.Nax[l][2];
     const double* A = P.A[l];
     for (int i = lane; i < n; i += 32) {
       const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
@@ -516,7 +515,10 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   LORPC_TRY(dense_coarse_setup(b, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
   // thread-per-patch V-cycle when the warp's 32 patch vectors fit in shared memory
-  b->tmode = b->Ld == 1 && b->max_n[1] <= 32 && tmode_smem(b) <= 227 * 1024 && 33ll * (b->max_n[0] + 1) < 65536;
+  // (level-1 boxes of at most 3 (3D) / 5 (2D) nodes per axis, see vcycle_t.cu TCoarse)
+  const int cext_max = (b->desc.patch_kind == 0 ? 2 : 3) * (lor->ml[1] - 1) - 1;
+  b->tmode = b->Ld == 1 && b->max_n[1] <= 32 && cext_max <= (d == 3 ? 3 : 5) && tmode_smem(b) <= 227 * 1024 &&
+             33ll * (b->max_n[0] + 1) < 65536;
   if (const char* e = getenv("LORPC_TMODE")) b->tmode = b->tmode && atoi(e) != 0;
   if (b->tmode) LORPC_TRY(trec_build(b, s));
   return LORPC_OK;

@@ -185,7 +185,7 @@ int trec_build(lorpc_prec* b, cudaStream_t s) {
   LORPC_LAUNCHED();
   LORPC_CUDA(cudaStreamSynchronize(s));
   dfree(b->Cd);
-  LORPC_TRY(dalloc(&b->zpark, (size_t)(nw * 2 * b->max_n[1] * 32)));
+  LORPC_TRY(dalloc(&b->zpark, (size_t)(nw * (3 * b->max_n[0] + 2 * b->max_n[1]) * 32)));
   return LORPC_OK;
 }
 
@@ -202,12 +202,12 @@ struct TcParams {
   long long J;
   const double* Cd;  // [warps][ldc][32] dense operator of the V-cycle on levels >= 1 (Ld = 1), lane q's
   int ldc;           //   column-major n1 x n1 matrix interleaved by patch
-  double* RZ;        // [warps][2][n1max][32] r_1 / z_1 of the warp's patches (global scratch)
+  double *xpark, *ypark, *spark;  // [warps][n0max][32] x, y, s of the warp's patches (lane columns)
+  double* rz;        // [warps][2][n1max][32] r_1, z_1
   int n1max;
   int n0max;         // largest finest-level patch (= the dummy node index)
-  int toff, r1off, z1off, voff;  // per-warp linear scratch: transfers, r_1, z_1, patch vector
-  int tpoff;                      // the warp's 32 patch geometries (TPatch)
-  int flags, pfd;                 // experiment switches (LORPC_TFLAGS), L2 prefetch distance (pair rows)
+  int tpoff;         // the warp's 32 patch geometries (TPatch)
+  int pfd;                        // L2 prefetch distance of the sweeps (pair rows)
   int warp_doubles;
   const double* r;
   double* z;
@@ -233,8 +233,8 @@ struct TStage {
 #define LORPC_TL_PAIR(P_)                                            \
   if ((P_) < NP) {                                                   \
     constexpr int pp = (P_) < NP ? (P_) : 0;                         \
-    if (2 * pp < cnt) s.l[pp] = __ldg(Lq + pp * 32);                 \
-    s.c[pp] = __ldg(Cq + pp * 32);                                   \
+    if (2 * pp < cnt) s.l[pp] = __ldcs(Lq + pp * 32);                \
+    s.c[pp] = __ldcs(Cq + pp * 32);                                  \
   }
 template <int NP>
 __device__ __forceinline__ void tload(TStage<NP>& s, const double2* __restrict__ Lp, const uint32_t* __restrict__ Cp,
@@ -396,124 +396,161 @@ __device__ __forceinline__ TPatch tpatch(const PatchGeom& G, long long j) {
   return c;
 }
 
-// Cooperative stencil pass over patch q's finest box, lanes over nodes.
-//  mode 0:  z += x_q (scatter), V[i] = r_i - (A x_q)_i          (x_q = X column q)
-//  mode 1:  z += V (scatter),   X[i, q] -= (A V)_i              (V = patch vector)
-//  mode 2:  z += x_q (scatter)
-// A_0 row of node g: NDP doubles at A0 + NDP g, loaded as 16-byte pairs.
-template <int DIM, int MODE>
-__device__ __forceinline__ void tpass(const TcParams& P, const TPatch& c, int X, int V, int q, int lane) {
+// ------------------------------------------------------------------ middle phase
+// Lane = patch, no shared memory (high occupancy); the patch vectors are the
+// lane's columns of warp-interleaved global buffers [warp][node][32] (every access
+// of a warp is one 256-byte row).  x: pre-smoothed iterate, y: after the coarse
+// correction, s: residual handed to the post-smoothing.
+
+// Thread mode: coarse-level box bound per axis (tmode requires n_1 <= 32)
+template <int DIM> struct TCoarse {
+  static constexpr int CX = DIM == 3 ? 3 : 5, CZ = DIM == 3 ? 3 : 1, NC = CX * CX * CZ;
+};
+
+// 1D restriction weights of fine node (ix, iy, iz) to the coarse box (dense W[c][f],
+// zero off the hat support)
+template <int DIM>
+__device__ __forceinline__ void tweights(const TcParams& P, const TPatch& c, int ix, int iy, int iz, double* wx,
+                                         double* wy, double* wz) {
+  constexpr int CX = TCoarse<DIM>::CX, CZ = TCoarse<DIM>::CZ;
+  const double* Wx = P.W + P.woff[c.ec[0]];
+  const double* Wy = P.W + P.woff[c.ec[1]];
+  const double* Wz = P.W + P.woff[DIM == 3 ? c.ec[2] : 1];
+#pragma unroll
+  for (int k = 0; k < CX; ++k) {
+    wx[k] = k < c.cext[0] ? __ldg(Wx + k * c.ext[0] + ix) : 0.0;
+    wy[k] = k < c.cext[1] ? __ldg(Wy + k * c.ext[1] + iy) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < CZ; ++k) wz[k] = DIM == 3 ? (k < c.cext[2] ? __ldg(Wz + k * c.ext[2] + iz) : 0.0) : 1.0;
+}
+
+// s_i = r_i - (A_0 v)_i at node i of the lane's patch, v = the lane's column V
+template <int DIM>
+__device__ __forceinline__ double tres_node(const TcParams& P, const TPatch& c, const double* __restrict__ V, int i,
+                                            int ix, int iy, int iz) {
   constexpr int ND = Dirs<DIM>::ND, NDP = Dirs<DIM>::NDP;
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2], n = c.n;
+  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+  const unsigned gi = (unsigned)((c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
+  const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
+  double a0 = __ldg(P.r + gi), a1 = 0.0;
+  const double2* Ar = (const double2*)(P.A0 + (size_t)gi * NDP);
+#pragma unroll
+  for (int d2 = 0; d2 < NDP / 2; ++d2) {
+    const double2 av = __ldg(Ar + d2);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int d = 2 * d2 + h;
+      if (d >= ND) break;
+      const int o = dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
+      const double v = (em & (1u << d)) ? V[(i + o) * 32] : 0.0;
+      if (h) a1 -= av.y * v; else a0 -= av.x * v;
+    }
+  }
+  return a0 + a1;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
+  constexpr int CX = TCoarse<DIM>::CX, CZ = TCoarse<DIM>::CZ, NC = TCoarse<DIM>::NC, NC1 = 32;
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long w = j >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= P.J) return;
+  const TPatch c = tpatch<DIM>(P.G, j);
+  const int n0 = P.n0max, ex = c.ext[0], ey = c.ext[1];
   const float rex = 1.0f / ex, rexy = 1.0f / (ex * ey);
-#pragma unroll 2
-  for (int i = lane; i < n; i += 32) {
+  const long long col = w * (long long)n0 * 32 + lane;
+  const double* Xp = P.xpark + col;
+  double* Yp = P.ypark + col;
+  double* Sp = P.spark + col;
+  // s = r - A x and r_1 = P^T s (fused)
+  double r1[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) r1[k] = 0.0;
+  for (int f = 0; f < c.n; ++f) {
     int ix, iy, iz;
-    box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
-    const unsigned gi = (unsigned)((c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
-    const int xi = X + VO(i, q), vi = V + i;
-    if (!(P.flags & 64)) atomicAdd(P.z + gi, MODE == 1 ? tsm[vi] : tsm[xi]);
-    if (MODE == 2) continue;
-    if (P.flags & 128) { if (MODE == 0) tsm[vi] = tsm[xi]; continue; }
-    const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
-    double a0 = MODE == 0 ? __ldg(P.r + gi) : tsm[xi], a1 = 0.0;
-    const double2* Ar = (const double2*)(P.A0 + (size_t)gi * NDP);
+    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    const double sv = tres_node<DIM>(P, c, Xp, f, ix, iy, iz);
+    double wx[CX], wy[CX], wz[CZ];
+    tweights<DIM>(P, c, ix, iy, iz, wx, wy, wz);
 #pragma unroll
-    for (int d2 = 0; d2 < NDP / 2; ++d2) {
-      const double2 av = __ldg(Ar + d2);
+    for (int kz = 0; kz < CZ; ++kz)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int d = 2 * d2 + h;
-        if (d >= ND) break;
-        const int o = dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
-        double v = 0.0;
-        if (em & (1u << d)) v = MODE == 0 ? tsm[xi + 33 * o] : tsm[vi + o];
-        if (h) a1 -= av.y * v; else a0 -= av.x * v;
+      for (int ky = 0; ky < CX; ++ky) {
+        const double wv = wy[ky] * wz[kz] * sv;
+#pragma unroll
+        for (int kx = 0; kx < CX; ++kx) r1[kx + CX * (ky + CX * kz)] += wx[kx] * wv;
       }
+  }
+  // z_1 = C r_1: r_1 to the patch's coarse numbering, C interleaved by lane
+  const int n1 = c.n1, cx = c.cext[0], cy = c.cext[1], cz = c.cext[2];
+  double* R = P.rz + w * 2ll * P.n1max * 32 + lane;
+  double* Z = R + P.n1max * 32;
+#pragma unroll
+  for (int kz = 0; kz < CZ; ++kz)
+#pragma unroll
+    for (int ky = 0; ky < CX; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < CX; ++kx)
+        if (kx < cx && ky < cy && kz < cz) R[(kx + cx * (ky + cy * kz)) * 32] = r1[kx + CX * (ky + CX * kz)];
+  {
+    const double* C = P.Cd + w * 32ll * P.ldc + lane;
+    double zc[NC1];
+#pragma unroll
+    for (int i = 0; i < NC1; ++i) zc[i] = 0.0;
+    for (int k = 0; k < n1; ++k) {
+      const double rk = R[k * 32];
+      const double* Ck = C + (long long)k * n1 * 32;
+#pragma unroll
+      for (int i = 0; i < NC1; ++i)
+        if (i < n1) zc[i] += __ldcs(Ck + i * 32) * rk;
     }
-    if (MODE == 0) tsm[vi] = a0 + a1; else tsm[xi] = a0 + a1;
+#pragma unroll
+    for (int i = 0; i < NC1; ++i)
+      if (i < n1) Z[i * 32] = zc[i];
+  }
+  // y = x + P z_1
+  double z1[NC];
+#pragma unroll
+  for (int kz = 0; kz < CZ; ++kz)
+#pragma unroll
+    for (int ky = 0; ky < CX; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < CX; ++kx)
+        z1[kx + CX * (ky + CX * kz)] = (kx < cx && ky < cy && kz < cz) ? Z[(kx + cx * (ky + cy * kz)) * 32] : 0.0;
+  for (int f = 0; f < c.n; ++f) {
+    int ix, iy, iz;
+    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    double wx[CX], wy[CX], wz[CZ];
+    tweights<DIM>(P, c, ix, iy, iz, wx, wy, wz);
+    double t = 0.0;
+#pragma unroll
+    for (int kz = 0; kz < CZ; ++kz)
+#pragma unroll
+      for (int ky = 0; ky < CX; ++ky) {
+        double u = 0.0;
+#pragma unroll
+        for (int kx = 0; kx < CX; ++kx) u += wx[kx] * z1[kx + CX * (ky + CX * kz)];
+        t += wy[ky] * wz[kz] * u;
+      }
+    Yp[f * 32] = Xp[f * 32] + t;
+  }
+  // s = r - A y
+  for (int f = 0; f < c.n; ++f) {
+    int ix, iy, iz;
+    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    __stcs(Sp + f * 32, tres_node<DIM>(P, c, Yp, f, ix, iy, iz));
   }
 }
 
-// r_1 = P^T x_q (separable: x, y[, z] passes through the scratch T)
-template <int DIM>
-__device__ __forceinline__ void trestrict(const TcParams& P, const TPatch& c, int X, int q, int lane) {
-  const int fx = c.ext[0], fy = c.ext[1], fz = c.ext[2], cx = c.cext[0], cy = c.cext[1], cz = c.cext[2];
-  const double* Wx = P.W + P.woff[c.ec[0]];
-  const double* Wy = P.W + P.woff[c.ec[1]];
-  const double* Wz = P.W + P.woff[DIM == 3 ? c.ec[2] : 1];
-  const int T = P.toff, Y = P.r1off;
-  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy);
-  for (int u = lane; u < cx * fy * fz; u += 32) {
-    const int rest = qdiv(u, rcx), ic = u - rest * cx;
-    double a = 0.0;
-    for (int f = 0; f < fx; ++f) a += __ldg(Wx + ic * fx + f) * tsm[X + VO(f + fx * rest, q)];
-    tsm[T + u] = a;
-  }
-  __syncwarp();
-  const int T2 = DIM == 3 ? T + cx * fy * fz : Y;
-  for (int u = lane; u < cx * cy * fz; u += 32) {
-    const int kf = qdiv(u, rcxy), r2 = u - kf * cx * cy, jc = qdiv(r2, rcx), ic = r2 - jc * cx;
-    double a = 0.0;
-    for (int f = 0; f < fy; ++f) a += __ldg(Wy + jc * fy + f) * tsm[T + ic + cx * (f + fy * kf)];
-    tsm[T2 + u] = a;
-  }
-  __syncwarp();
-  if (DIM == 3) {
-    for (int u = lane; u < cx * cy * cz; u += 32) {
-      const int kc = qdiv(u, rcxy), ij = u - kc * cx * cy;
-      double a = 0.0;
-      for (int f = 0; f < fz; ++f) a += __ldg(Wz + kc * fz + f) * tsm[T2 + ij + cx * cy * f];
-      tsm[Y + u] = a;
-    }
-    __syncwarp();
-  }
-}
-
-// V = P z_1 (finest box of patch q, linear)
-template <int DIM>
-__device__ __forceinline__ void tprolong(const TcParams& P, const TPatch& c, int lane) {
-  const int fx = c.ext[0], fy = c.ext[1], fz = c.ext[2], cx = c.cext[0], cy = c.cext[1], cz = c.cext[2];
-  const double* Wx = P.W + P.woff[c.ec[0]];
-  const double* Wy = P.W + P.woff[c.ec[1]];
-  const double* Wz = P.W + P.woff[DIM == 3 ? c.ec[2] : 1];
-  const int T = P.toff, E = P.z1off, V = P.voff;
-  const float rcx = 1.0f / cx, rcxy = 1.0f / (cx * cy), rcxfy = 1.0f / (cx * fy), rfx = 1.0f / fx;
-  int U2 = E;
-  if (DIM == 3) {
-    U2 = T + cx * fy * fz;
-    for (int u = lane; u < cx * cy * fz; u += 32) {
-      const int kf = qdiv(u, rcxy), ij = u - kf * cx * cy;
-      double a = 0.0;
-      for (int cc = 0; cc < cz; ++cc) a += __ldg(Wz + cc * fz + kf) * tsm[E + ij + cx * cy * cc];
-      tsm[U2 + u] = a;
-    }
-    __syncwarp();
-  }
-  for (int u = lane; u < cx * fy * fz; u += 32) {
-    const int kf = qdiv(u, rcxfy), r2 = u - kf * cx * fy, jf = qdiv(r2, rcx), ic = r2 - jf * cx;
-    double a = 0.0;
-    for (int cc = 0; cc < cy; ++cc) a += __ldg(Wy + cc * fy + jf) * tsm[U2 + ic + cx * (cc + cy * kf)];
-    tsm[T + u] = a;
-  }
-  __syncwarp();
-  for (int i = lane; i < c.n; i += 32) {
-    const int rest = qdiv(i, rfx), fxi = i - rest * fx;
-    double a = 0.0;
-    for (int cc = 0; cc < cx; ++cc) a += __ldg(Wx + cc * fx + fxi) * tsm[T + cc + cx * rest];
-    tsm[V + i] = a;
-  }
-  __syncwarp();
-}
-
-// One V(1,1) cycle per patch (a6) with the levels >= 1 folded into the dense
-// operator C_j (Ld = 1):  z_j = x + t + c with
-//   x = M_0^{-1} r_j,  s = r_j - A_0 x,  t = P_0 C_j P_0^T s,  c = M_0^{-1} (s - A_0 t),
-// each of x, t, c added to z as soon as it is final (z += I_j z_j, a8).
-template <int DIM>
-__global__ void __launch_bounds__(32) k_vcycle_t(TcParams P) {
-  constexpr int NP = DIM == 3 ? 13 : 4, NC1 = 32;
+// ------------------------------------------------------------------ smoothing phases
+// pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
+// post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
+template <int DIM, bool POST>
+__global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
+  constexpr int NP = DIM == 3 ? 13 : 4;
   const int lane = threadIdx.x;
   const long long w = blockIdx.x;
   const int X = 0, n0 = P.n0max;
@@ -522,70 +559,40 @@ __global__ void __launch_bounds__(32) k_vcycle_t(TcParams P) {
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
   TPatch* tpa = (TPatch*)(tsm + P.tpoff);
   if (lane < nq) tpa[lane] = tpatch<DIM>(P.G, w * 32 + lane);
-  __syncwarp();
-  // r_j = I_j^T r (a5)
-  for (int q = 0; q < nq; ++q) {
-    const TPatch c = tpa[q];
-    const float rex = 1.0f / c.ext[0], rexy = 1.0f / (c.ext[0] * c.ext[1]);
-    for (int i = lane; i < c.n; i += 32) {
-      int ix, iy, iz;
-      box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
-      tsm[X + VO(i, q)] = __ldg(P.r + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
+  const long long col = w * (long long)n0 * 32 + lane;
+  if (!POST) {
+    __syncwarp();
+    for (int q = 0; q < nq; ++q) {  // r_j = I_j^T r (a5)
+      const TPatch c = tpa[q];
+      const float rex = 1.0f / c.ext[0], rexy = 1.0f / (c.ext[0] * c.ext[1]);
+      for (int i = lane; i < c.n; i += 32) {
+        int ix, iy, iz;
+        box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
+        tsm[X + VO(i, q)] = __ldg(P.r + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
+      }
     }
+  } else {
+    for (int i = 0; i < n0; ++i) tsm[X + VO(i, lane)] = __ldcs(P.spark + col + i * 32);
   }
   tsm[X + VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
 #pragma unroll 1
-  for (int ph = 0; ph < 2; ++ph) {
-    // ph 0: x = M^{-1} r_j (pre-smoothing);  ph 1: c = M^{-1} s (post-smoothing)
-#pragma unroll 1
-    for (int sw = 0; sw < 2; ++sw)
-      if (!(P.flags & 4)) tsweep<NP>(blk, X, n0, sw == 1, P.pfd, lane);
+  for (int sw = 0; sw < 2; ++sw) tsweep<NP>(blk, X, n0, sw == 1, P.pfd, lane);
+  if (!POST) {
+    for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[X + VO(i, lane)]);
+  } else {
+    for (int i = 0; i < n0; ++i) tsm[X + VO(i, lane)] += __ldcs(P.ypark + col + i * 32);
     __syncwarp();
-    if (ph == 1) break;
-    if (P.flags & 2) continue;
-    double* Rg = P.RZ + w * (2ll * P.n1max * 32);
-    double* Zg = Rg + P.n1max * 32;
-    for (int q = 0; q < nq; ++q) {
+    for (int q = 0; q < nq; ++q) {  // z += I_j z_j (a8), lanes over consecutive nodes
       const TPatch c = tpa[q];
-      if (!(P.flags & 8)) tpass<DIM, 0>(P, c, X, P.voff, q, lane);      // z += x; s = r - A x  (into V)
-      __syncwarp();
-      for (int i = lane; i < c.n; i += 32) tsm[X + VO(i, q)] = tsm[P.voff + i];
-      __syncwarp();
-      if (!(P.flags & 16)) trestrict<DIM>(P, c, X, q, lane);             // r_1 = P^T s
-      for (int k = lane; k < c.n1; k += 32) Rg[k * 32 + q] = tsm[P.r1off + k];
-    }
-    __syncwarp();
-    {  // z_1 = C r_1, lane = patch, z_1 in registers
-      const int n1 = lane < nq ? tpa[lane].n1 : 0;
-      const double* C = P.Cd + w * 32ll * P.ldc + lane;
-      double zc[NC1];
-#pragma unroll
-      for (int i = 0; i < NC1; ++i) zc[i] = 0.0;
-      for (int k = 0; k < ((P.flags & 32) ? 0 : n1); ++k) {
-        const double rk = Rg[k * 32 + lane];
-        const double* Ck = C + (long long)k * n1 * 32;
-#pragma unroll
-        for (int i = 0; i < NC1; ++i)
-          if (i < n1) zc[i] += __ldg(Ck + i * 32) * rk;
+      const float rex = 1.0f / c.ext[0], rexy = 1.0f / (c.ext[0] * c.ext[1]);
+      for (int i = lane; i < c.n; i += 32) {
+        int ix, iy, iz;
+        box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
+        atomicAdd(P.z + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)),
+                  tsm[X + VO(i, q)]);
       }
-#pragma unroll
-      for (int i = 0; i < NC1; ++i)
-        if (i < n1) Zg[i * 32 + lane] = zc[i];
     }
-    __syncwarp();
-    for (int q = 0; q < nq; ++q) {
-      const TPatch c = tpa[q];
-      for (int k = lane; k < c.n1; k += 32) tsm[P.z1off + k] = Zg[k * 32 + q];
-      __syncwarp();
-      if (!(P.flags & 16)) tprolong<DIM>(P, c, lane);                    // t = P z_1  (into V)
-      if (!(P.flags & 8)) tpass<DIM, 1>(P, c, X, P.voff, q, lane);      // z += t; s -= A t
-      __syncwarp();
-    }
-  }
-  for (int q = 0; q < nq; ++q) {
-    const TPatch c = tpa[q];
-    tpass<DIM, 2>(P, c, X, 0, q, lane);           // z += c
   }
 }
 
@@ -597,17 +604,13 @@ static TcParams make_tparams(const lorpc_prec* b, const double* r, double* z) {
   memcpy(P.woff, b->woff[0], sizeof(P.woff));
   P.trec = b->trec; P.trecoff = b->trecoff; P.J = b->J;
   P.Cd = b->Cdi; P.ldc = b->ldc;
-  P.RZ = b->zpark; P.n1max = b->max_n[1];
+  P.n0max = b->max_n[0]; P.n1max = b->max_n[1];
+  const long long nw = (b->J + 31) / 32, pcol = nw * b->max_n[0] * 32;
+  P.xpark = b->zpark; P.ypark = b->zpark + pcol; P.spark = b->zpark + 2 * pcol; P.rz = b->zpark + 3 * pcol;
   P.r = r; P.z = z;
-  P.n0max = b->max_n[0];
   int acc = VO(b->max_n[0] + 1, 0);
-  P.toff = acc; acc += b->scratch_doubles;
-  P.r1off = acc; acc += b->max_n[1];
-  P.z1off = acc; acc += b->max_n[1];
-  P.voff = acc; acc += b->max_n[0];
   P.tpoff = acc; acc += 32 * (int)(sizeof(TPatch) / sizeof(double));
   P.warp_doubles = (acc + 1) & ~1;
-  P.flags = getenv("LORPC_TFLAGS") ? atoi(getenv("LORPC_TFLAGS")) : 0;
   P.pfd = getenv("LORPC_TPFD") ? atoi(getenv("LORPC_TPFD")) : 32;
   return P;
 }
@@ -620,13 +623,23 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   const TcParams P = make_tparams(b, r, z);
   const size_t smem = (size_t)P.warp_doubles * sizeof(double);
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
-  const unsigned blocks = (unsigned)((b->J + 31) / 32);
+  const unsigned wblocks = (unsigned)((b->J + 31) / 32), mblocks = (unsigned)((b->J + 127) / 128);
   if (b->m->d == 2) {
-    cudaFuncSetAttribute(k_vcycle_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_vcycle_t<2><<<blocks, 32, smem, s>>>(P);
+    cudaFuncSetAttribute(k_vt_smooth<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_vt_smooth<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_vt_smooth<2, false><<<wblocks, 32, smem, s>>>(P);
+    LORPC_LAUNCHED();
+    k_vt_mid<2><<<mblocks, 128, 0, s>>>(P);
+    LORPC_LAUNCHED();
+    k_vt_smooth<2, true><<<wblocks, 32, smem, s>>>(P);
   } else {
-    cudaFuncSetAttribute(k_vcycle_t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_vcycle_t<3><<<blocks, 32, smem, s>>>(P);
+    cudaFuncSetAttribute(k_vt_smooth<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_vt_smooth<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_vt_smooth<3, false><<<wblocks, 32, smem, s>>>(P);
+    LORPC_LAUNCHED();
+    k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
+    LORPC_LAUNCHED();
+    k_vt_smooth<3, true><<<wblocks, 32, smem, s>>>(P);
   }
   LORPC_LAUNCHED();
   return LORPC_OK;
