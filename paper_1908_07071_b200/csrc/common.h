@@ -125,7 +125,8 @@ struct lorpc_prec {
   long long* trecoff = nullptr;
   long long trec_bytes = 0;
   double* zpark = nullptr;          // per-warp r_1 / z_1 scratch
-  double* Cdi = nullptr;            // dense coarse operators, interleaved by patch per warp
+  double* Cdi = nullptr;            // dense coarse operators, packed symmetric, interleaved by patch per warp
+  int* pord = nullptr;
   // coarse space (R_0)
   int nc = 0;                       // GMG levels
   int cn[lorpc::MAXC][3];           // vertices per axis

@@ -1,21 +1,19 @@
 // Thread-per-patch Schwarz V-cycle (rows a5, a6, a8; "patches are
 // processed independently and batched").
 //
-// One lane owns one patch, one warp owns 32 consecutive patches.  The MDF-ordered
-// ILU(0) sweeps, a strictly sequential chain per patch, run lane-parallel over
-// the warp's 32 patches with no synchronisation and no reductions: lane q walks
-// its own patch's rows in elimination-schedule order.  The factors are stored
-// warp-interleaved ("T-records", built from the per-patch records at setup) so
-// that every load of a sweep step is one coalesced 256-byte row; the step is
-// padded to the warp's widest row and the padding lanes are predicated off (no
-// memory traffic).  The stencil phases (gather, residual, transfers, dense coarse
-// operator, scatter) are cooperative: all 32 lanes work on one patch at a time.
+// One lane owns one patch, one warp owns 32 patches.  The MDF-ordered ILU(0)
+// sweeps, a strictly sequential chain per patch, run lane-parallel over the warp's
+// 32 patches with no synchronisation and no reductions: lane q walks its own
+// patch's rows in its DAG-schedule order.  The factors are stored warp-interleaved
+// ("T-records", built from the per-patch records at setup) so that every load of a
+// sweep step is one coalesced row; a step is padded to the warp's widest column
+// and the padding lanes are predicated off (no memory traffic).
 //
-// Shared memory per warp: vector X of the 32 patches is laid out [node][patch]
-// with an XOR swizzle, element (i, q) at X + 32 i + (q ^ (i & 15)), so that both
-// the sweeps (lanes = patches, arbitrary rows) and the cooperative phases (lanes
-// = consecutive nodes of one patch) are free of bank conflicts within a
-// half-warp (the sweeps up to the random row collisions of the MDF orderings).
+// Three kernels per apply: pre-smoothing (gather r_j = I_j^T r, x = M^{-1} r_j),
+// the coarse correction (lane = patch: s = r_j - A x, r_1 = P^T s, z_1 = C r_1
+// with C the dense V-cycle operator of levels >= 1, y = x + P z_1, s = r_j - A y)
+// and post-smoothing (z_j = y + M^{-1} s, scatter z += I_j z_j).  The patch
+// vectors travel between them in warp-interleaved "park" buffers [warp][node][32].
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -25,352 +23,125 @@
 
 namespace lorpc {
 
+// ------------------------------------------------------------------ warp slots
+// Warp w owns the patches pord[32 w .. 32 w + 31] (-1: empty slot, only in the
+// last warp).  The patch grid is walked in tiles of TX x TY patch columns, each
+// tile bottom to top (z outer), so that patches sharing LOR rows and r / z entries
+// run at nearly the same time and meet in L2: z-neighbours are one tile layer
+// (TX * TY patches) apart, while lexicographic order puts them a whole patch plane
+// apart, beyond the L2 reuse window of the concurrently resident warps.
+static std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
+  const lorpc_mesh* m = b->m;
+  const int d = m->d, star = b->desc.patch_kind == 1;
+  const int gx = m->n[0] + (star ? 0 : 1), gy = m->n[1] + (star ? 0 : 1);
+  const int gz = d == 3 ? m->n[2] + (star ? 0 : 1) : 1;
+  const long long nw = (b->J + 31) / 32;
+  std::vector<int> ord;
+  ord.reserve((size_t)(nw * 32));
+  for (int y0 = 0; y0 < gy; y0 += TY)
+    for (int x0 = 0; x0 < gx; x0 += TX)
+      for (int z = 0; z < gz; ++z)
+        for (int y = y0; y < std::min(y0 + TY, gy); ++y)
+          for (int x = x0; x < std::min(x0 + TX, gx); ++x) ord.push_back(x + gx * (y + gy * z));
+  ord.resize((size_t)(nw * 32), -1);
+  return ord;
+}
+
 // ------------------------------------------------------------------ T-records
-// Block of (warp w, level 0) at trecoff[w], 256-byte aligned:
-//   int4 {S, Kf, Kb, 0}: S steps (largest patch of the warp), Kf / Kb entry slots
-//   hdr[S][32] u32   VO(node) | cf << 16 | cb << 24 of the row of step t (schedule order)
-//   D[S][32]   f64   its pivot
-//   Lf[Kf/2][32][2] f64, Lb[Kb/2][32][2] f64   forward L_ij / backward L_ki, in
-//                    entry pairs (one 16-byte load per lane and pair)
-//   Cf[Kf/2][32][2] u16, Cb[Kb/2][32][2] u16   VO of their neighbour node j / k
-// Step t of the forward sweep owns the pair rows [sum_{t'<t} mp_t', + mp_t) with
-// mp_t = max over the warp's lanes of ceil(cf / 2); the backward sweep likewise.
-// Shared-memory layout of the warp's 32 patch vectors: node i of patch (lane) q at
-// word VO(i, q) = 33 i + q, conflict-free for lanes = patches at one node and for
-// lanes = consecutive nodes of one patch.  The T-records store these word offsets
-// (lane-specific) instead of node numbers.
-#define VO(i, q) ((i) * 33 + (q))
-struct TRecLayout { long long hdr, D, Lf, Lb, Cf, Cb, total; };
+// Block of (warp w, level 0) at trecoff[w], 256-byte aligned.  Step t of lane q
+// stores the COLUMN of its node k: the entries L_ik of the later neighbours i.  The
+// forward sweep pushes (y_i -= L_ik y_k, then x_k = y_k / D_k) and the backward
+// sweep pulls (x_k -= sum_i L_ik x_i, steps descending) from the same data, so the
+// factor is stored once and the backward sweep re-reads, in reverse, what the
+// forward sweep has just pulled through L2:
+//   int4 {S, Kp, 0, 0}: S steps (largest patch of the warp), Kp pair rows
+//   hdr[S][32]  u32  node k (bits 0-7) | count (bits 8-15) | mp (bits 16-23): pair
+//                    rows of step t (the warp maximum, the same in every lane)
+//   Dinv[S][32] f64  1 / D_k
+//   Lc[Kp][32]  f64x2 column entries in pairs (one 16-byte load per lane and pair)
+//   Ic[Kp][32]  u8x2  their node indices i
+// Padding entries carry L = 0 and the dummy node n0max, padding steps the dummy
+// node with count 0 (node indices are u8: thread mode requires n0max <= 254).
+struct TRecLayout { long long hdr, D, Lc, Ic, total; };
 __host__ __device__ __forceinline__ long long a256(long long b) { return (b + 255) & ~255ll; }
-__host__ __device__ __forceinline__ TRecLayout trec_layout(int S, int Kf, int Kb) {
+__host__ __device__ __forceinline__ TRecLayout trec_layout(int S, int Kp) {
   TRecLayout T;
   T.hdr = 256;
   T.D = a256(T.hdr + 128ll * S);
-  T.Lf = T.D + 256ll * S;
-  T.Lb = T.Lf + 256ll * Kf;
-  T.Cf = T.Lb + 256ll * Kb;
-  T.Cb = T.Cf + 64ll * Kf;
-  T.total = a256(T.Cb + 64ll * Kb);
+  T.Lc = T.D + 256ll * S;
+  T.Ic = T.Lc + 512ll * Kp;
+  T.total = a256(T.Ic + 64ll * Kp);
   return T;
 }
 
 struct TRecParams {
   const char* rec;
   const long long* recoff;
-  long long J;
-  int L, Ld;
-  int dummy[MAXL];
+  const int* pord;
+  int L;
+  int dummy;
   long long* sizes;
   char* trec;
   const long long* trecoff;
 };
 
-// fill = 0: block sizes; fill = 1: write the blocks.  Thread = patch.
-__global__ void __launch_bounds__(128) k_trec(TRecParams P, int fill) {
-  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long w = j >> 5;
+// fill = 0: block sizes; fill = 1: write the blocks.  Thread = warp slot.
+__global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, int fill) {
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((slot & ~31ll) >= nslots) return;  // warp-uniform
+  const long long w = slot >> 5;
   const int lane = threadIdx.x & 31;
-  if ((w << 5) >= P.J) return;  // warp-uniform
-  for (int l = 0; l < P.Ld; ++l) {
-    int n = 0, nL = 0;
-    const char* rec = P.rec;
-    if (j < P.J) {
-      rec = P.rec + P.recoff[j * P.L + l];
-      const int4 h = *(const int4*)rec;
-      n = h.x; nL = h.z;
-    }
-    const RecLayout R = rec_layout(n, nL);
-    const uint16_t* frp = (const uint16_t*)(rec + R.frp);
-    const uint16_t* brp = (const uint16_t*)(rec + R.brp);
-    const int S = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
-    int Kf = 0, Kb = 0;
-    for (int t = 0; t < S; ++t) {
-      const unsigned cf = t < n ? frp[t + 1] - frp[t] : 0u, cb = t < n ? brp[t + 1] - brp[t] : 0u;
-      Kf += 2 * (int)__reduce_max_sync(0xffffffffu, (cf + 1) / 2);
-      Kb += 2 * (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
-    }
-    const TRecLayout T = trec_layout(S, Kf, Kb);
-    if (!fill) {
-      if (lane == 0) P.sizes[w * P.Ld + l] = T.total;
-      continue;
-    }
-    char* blk = P.trec + P.trecoff[w * P.Ld + l];
-    if (lane == 0) *(int4*)blk = make_int4(S, Kf, Kb, 0);
-    uint32_t* H = (uint32_t*)(blk + T.hdr);
-    double* Dd = (double*)(blk + T.D);
-    double* Lf = (double*)(blk + T.Lf);
-    double* Lb = (double*)(blk + T.Lb);
-    uint16_t* Cf = (uint16_t*)(blk + T.Cf);
-    uint16_t* Cb = (uint16_t*)(blk + T.Cb);
-    const double* Dn = (const double*)(rec + R.D);
-    const double* Lv = (const double*)(rec + R.L);
-    const uint16_t* nbv = (const uint16_t*)(rec + R.nb);
-    const double* bLv = (const double*)(rec + R.bL);
-    const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
-    const uint16_t* sch = (const uint16_t*)(rec + R.sched);
-    const int dummy = VO(P.dummy[l], lane);
-    int kf = 0, kb = 0;
-    for (int t = 0; t < S; ++t) {
-      int node = dummy, f0 = 0, b0 = 0;
-      unsigned cf = 0, cb = 0;
-      double dv = 1.0;
-      if (t < n) {
-        node = VO(sch[t], lane);
-        f0 = frp[t]; cf = frp[t + 1] - f0;
-        b0 = brp[t]; cb = brp[t + 1] - b0;
-        dv = Dn[sch[t]];
-      }
-      H[t * 32 + lane] = (uint32_t)node | (cf << 16) | (cb << 24);
-      Dd[t * 32 + lane] = dv;
-      const int mf = 2 * (int)__reduce_max_sync(0xffffffffu, (cf + 1) / 2);
-      for (int k = 0; k < mf; ++k) {
-        const bool in = k < (int)cf;
-        const long long ix = ((long long)(kf + k) / 2 * 32 + lane) * 2 + (k & 1);
-        Lf[ix] = in ? Lv[f0 + k] : 0.0;
-        Cf[ix] = (uint16_t)(in ? VO(nbv[f0 + k], lane) : dummy);
-      }
-      kf += mf;
-      const int mb = 2 * (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
-      for (int k = 0; k < mb; ++k) {
-        const bool in = k < (int)cb;
-        const long long ix = ((long long)(kb + k) / 2 * 32 + lane) * 2 + (k & 1);
-        Lb[ix] = in ? bLv[b0 + k] : 0.0;
-        Cb[ix] = (uint16_t)(in ? VO(bkv[b0 + k], lane) : dummy);
-      }
-      kb += mb;
-    }
+  const long long j = P.pord[slot];
+  int n = 0, nL = 0;
+  const char* rec = P.rec;
+  if (j >= 0) {
+    rec = P.rec + P.recoff[j * P.L];
+    const int4 h = *(const int4*)rec;
+    n = h.x; nL = h.z;
   }
-}
-
-// Cdi[w][k][q] = Cd[32 w + q][k] (zero for q beyond J)
-__global__ void k_interleave_c(const double* __restrict__ Cd, double* __restrict__ Cdi, long long J, int ldc) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long nw = (J + 31) / 32;
-  if (t >= nw * 32 * ldc) return;
-  const int q = (int)(t % 32);
-  const long long k = (t / 32) % ldc, w = t / (32ll * ldc);
-  const long long j = w * 32 + q;
-  Cdi[t] = j < J ? Cd[j * ldc + k] : 0.0;
-}
-
-int trec_build(lorpc_prec* b, cudaStream_t s) {
-  const long long nw = (b->J + 31) / 32;
-  const int Ld = 1;  // T-records of the finest level only (thread mode requires Ld == 1)
-  TRecParams P{};
-  P.rec = b->rec; P.recoff = b->recoff; P.J = b->J; P.L = b->L; P.Ld = Ld;
-  for (int l = 0; l < b->L; ++l) P.dummy[l] = b->max_n[l];
-  long long* sizes = nullptr;
-  LORPC_TRY(dalloc(&sizes, (size_t)(nw * Ld)));
-  P.sizes = sizes;
-  const unsigned blocks = (unsigned)((nw * 32 + 127) / 128);
-  k_trec<<<blocks, 128, 0, s>>>(P, 0);
-  LORPC_LAUNCHED();
-  std::vector<long long> h((size_t)(nw * Ld));
-  LORPC_CUDA(cudaMemcpyAsync(h.data(), sizes, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
-  LORPC_CUDA(cudaStreamSynchronize(s));
-  long long off = 0;
-  for (auto& v : h) { const long long sz = v; v = off; off += sz; }
-  b->trec_bytes = off;
-  LORPC_TRY(dalloc(&b->trec, (size_t)off));
-  LORPC_TRY(dalloc(&b->trecoff, h.size()));
-  LORPC_CUDA(cudaMemcpyAsync(b->trecoff, h.data(), sizeof(long long) * h.size(), cudaMemcpyHostToDevice, s));
-  P.trec = b->trec; P.trecoff = b->trecoff;
-  k_trec<<<blocks, 128, 0, s>>>(P, 1);
-  LORPC_LAUNCHED();
-  LORPC_CUDA(cudaStreamSynchronize(s));
-  dfree(sizes);
-  // dense coarse operators interleaved by patch within each warp; r_1 / z_1 scratch
-  LORPC_TRY(dalloc(&b->Cdi, (size_t)(nw * 32 * b->ldc)));
-  k_interleave_c<<<nb(nw * 32 * b->ldc, 256), 256, 0, s>>>(b->Cd, b->Cdi, b->J, b->ldc);
-  LORPC_LAUNCHED();
-  LORPC_CUDA(cudaStreamSynchronize(s));
-  dfree(b->Cd);
-  LORPC_TRY(dalloc(&b->zpark, (size_t)(nw * (3 * b->max_n[0] + 2 * b->max_n[1]) * 32)));
-  return LORPC_OK;
-}
-
-// ------------------------------------------------------------------ kernel
-extern __shared__ __align__(16) double tsm[];
-
-struct TcParams {
-  PatchGeom G;
-  const double* A0;  // finest LOR level, node-major rows of NDP doubles
-  const double* W;   // separable restriction tables, level 0 -> 1
-  int woff[4];
-  const char* trec;
-  const long long* trecoff;
-  long long J;
-  const double* Cd;  // [warps][ldc][32] dense operator of the V-cycle on levels >= 1 (Ld = 1), lane q's
-  int ldc;           //   column-major n1 x n1 matrix interleaved by patch
-  double *xpark, *ypark, *spark;  // [warps][n0max][32] x, y, s of the warp's patches (lane columns)
-  double* rz;        // [warps][2][n1max][32] r_1, z_1
-  int n1max;
-  int n0max;         // largest finest-level patch (= the dummy node index)
-  int tpoff;         // the warp's 32 patch geometries (TPatch)
-  int pfd;                        // L2 prefetch distance of the sweeps (pair rows)
-  int warp_doubles;
-  const double* r;
-  double* z;
-};
-
-__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-
-// One sweep step's factor data, register-resident (NP = max entry pairs per row)
-template <int NP>
-struct TStage {
-  double2 l[NP];
-  uint32_t c[NP];
-};
-// Loads of one step: mp pair rows (warp-uniform) from row kp.  Lanes whose row
-// is shorter skip the value loads of their padding pairs (no memory traffic);
-// their stale register values meet the zero at the dummy node in tdot, so the
-// stage must start finite (zeroed).  The neighbour offsets are always loaded
-// (padding holds the dummy).  Entered by a jump into a fall-through sequence
-// instead of one branch per pair.
-#define LORPC_TL_PAIR(P_)                                            \
-  if ((P_) < NP) {                                                   \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                         \
-    if (2 * pp < cnt) s.l[pp] = __ldcs(Lq + pp * 32);                \
-    s.c[pp] = __ldcs(Cq + pp * 32);                                  \
+  const RecLayout R = rec_layout(n, nL);
+  const uint16_t* brp = (const uint16_t*)(rec + R.brp);
+  const int S = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+  int Kp = 0;
+  for (int t = 0; t < S; ++t) {
+    const unsigned cb = t < n ? brp[t + 1] - brp[t] : 0u;
+    Kp += (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
   }
-template <int NP>
-__device__ __forceinline__ void tload(TStage<NP>& s, const double2* __restrict__ Lp, const uint32_t* __restrict__ Cp,
-                                      int kp, int mp, int cnt) {
-  const double2* Lq = Lp + (long long)kp * 32;
-  const uint32_t* Cq = Cp + (long long)kp * 32;
-  switch (mp) {
-    case 13: LORPC_TL_PAIR(12); [[fallthrough]];
-    case 12: LORPC_TL_PAIR(11); [[fallthrough]];
-    case 11: LORPC_TL_PAIR(10); [[fallthrough]];
-    case 10: LORPC_TL_PAIR(9); [[fallthrough]];
-    case 9: LORPC_TL_PAIR(8); [[fallthrough]];
-    case 8: LORPC_TL_PAIR(7); [[fallthrough]];
-    case 7: LORPC_TL_PAIR(6); [[fallthrough]];
-    case 6: LORPC_TL_PAIR(5); [[fallthrough]];
-    case 5: LORPC_TL_PAIR(4); [[fallthrough]];
-    case 4: LORPC_TL_PAIR(3); [[fallthrough]];
-    case 3: LORPC_TL_PAIR(2); [[fallthrough]];
-    case 2: LORPC_TL_PAIR(1); [[fallthrough]];
-    case 1: LORPC_TL_PAIR(0); [[fallthrough]];
-    default: break;
+  const TRecLayout T = trec_layout(S, Kp);
+  if (!fill) {
+    if (lane == 0) P.sizes[w] = T.total;
+    return;
   }
-}
-#undef LORPC_TL_PAIR
-#define LORPC_TD_PAIR(P_)                                            \
-  if ((P_) < NP) {                                                   \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                         \
-    a0 -= s.l[pp].x * tsm[X + (s.c[pp] & 0xffff)];                   \
-    a1 -= s.l[pp].y * tsm[X + (s.c[pp] >> 16)];                      \
-  }
-template <int NP>
-__device__ __forceinline__ double tdot(const TStage<NP>& s, int mp, double a0, int X) {
-  double a1 = 0.0;
-  switch (mp) {
-    case 13: LORPC_TD_PAIR(12); [[fallthrough]];
-    case 12: LORPC_TD_PAIR(11); [[fallthrough]];
-    case 11: LORPC_TD_PAIR(10); [[fallthrough]];
-    case 10: LORPC_TD_PAIR(9); [[fallthrough]];
-    case 9: LORPC_TD_PAIR(8); [[fallthrough]];
-    case 8: LORPC_TD_PAIR(7); [[fallthrough]];
-    case 7: LORPC_TD_PAIR(6); [[fallthrough]];
-    case 6: LORPC_TD_PAIR(5); [[fallthrough]];
-    case 5: LORPC_TD_PAIR(4); [[fallthrough]];
-    case 4: LORPC_TD_PAIR(3); [[fallthrough]];
-    case 3: LORPC_TD_PAIR(2); [[fallthrough]];
-    case 2: LORPC_TD_PAIR(1); [[fallthrough]];
-    case 1: LORPC_TD_PAIR(0); [[fallthrough]];
-    default: break;
-  }
-  return a0 + a1;
-}
-#undef LORPC_TD_PAIR
-
-// One triangular sweep of the lane's own patch over the T-record block: forward
-// (x_i -= sum_{j earlier} L_ij x_j, steps ascending) or backward with the
-// diagonal fused (x_i = x_i / D_i - sum_{k later} L_ki x_k, steps descending).
-// Software-pipelined one step deep (unrolled by two so that the register stages
-// swap roles without moves): the next step's factor rows are loaded while the
-// current one is applied, and the record streams through L2 prefetches TPFD pair
-// rows ahead.  The kernel instantiates it once (runtime direction, the two
-// smoothing steps in a loop), which keeps the kernel inside the instruction cache.
-template <int NP>
-__device__ __forceinline__ void tsweep(const char* __restrict__ blk, int X, int dummy, bool bwd, int TPFD, int lane) {
-  const int4 hd = __ldg((const int4*)blk);
-  const int S = hd.x;
-  if (S == 0) return;
-  const TRecLayout T = trec_layout(S, hd.y, hd.z);
-  const int Kp = (bwd ? hd.z : hd.y) / 2, sh = bwd ? 24 : 16, dir = bwd ? -32 : 32;
-  const uint32_t* H = (const uint32_t*)(blk + T.hdr) + lane + (bwd ? (S - 1) * 32 : 0);
-  const double* Dd = (const double*)(blk + T.D) + lane + (S - 1) * 32;
-  const double2* Lp = (const double2*)(blk + (bwd ? T.Lb : T.Lf)) + lane;
-  const uint32_t* Cp = (const uint32_t*)(blk + (bwd ? T.Cb : T.Cf)) + lane;
-  auto pairs = [&](uint32_t h) { return (int)__reduce_max_sync(0xffffffffu, (((h >> sh) & 0xffu) + 1u) >> 1); };
-  // L2 prefetch cursor (pair rows; forward ascending, backward descending)
-  int pf = 0;
-  auto prefetch = [&](int kp) {
-    if (lane != 0) return;
-    if (!bwd) {
-      while (pf < Kp && pf < kp + TPFD) {
-        const int nr = min(8, Kp - pf);
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-        l2_prefetch(Cp - lane + pf * 32, 128u * nr);
-        pf += nr;
-      }
-    } else {
-      while (pf > 0 && pf > kp - TPFD) {
-        const int nr = min(8, pf);
-        pf -= nr;
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-        l2_prefetch(Cp - lane + pf * 32, 128u * nr);
-      }
+  char* blk = P.trec + P.trecoff[w];
+  if (lane == 0) *(int4*)blk = make_int4(S, Kp, 0, 0);
+  uint32_t* H = (uint32_t*)(blk + T.hdr);
+  double* Dd = (double*)(blk + T.D);
+  double* Lc = (double*)(blk + T.Lc);
+  uint8_t* Ic = (uint8_t*)(blk + T.Ic);
+  const double* Dn = (const double*)(rec + R.D);
+  const double* bLv = (const double*)(rec + R.bL);
+  const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  int kp = 0;
+  for (int t = 0; t < S; ++t) {
+    int node = P.dummy, b0 = 0;
+    unsigned cb = 0;
+    double dv = 1.0;
+    if (t < n) {
+      node = sch[t];
+      b0 = brp[t]; cb = brp[t + 1] - b0;
+      dv = 1.0 / Dn[node];
     }
-  };
-  if (lane == 0) {
-    l2_prefetch((const uint32_t*)(blk + T.hdr), 128u * S);
-    if (bwd) l2_prefetch((const double*)(blk + T.D), 256u * S);
-    pf = bwd ? Kp : 0;
-  }
-  TStage<NP> A, B;
-#pragma unroll
-  for (int p = 0; p < NP; ++p) A.l[p] = B.l[p] = make_double2(0.0, 0.0);
-  uint32_t h0 = __ldg(H), h1 = S > 1 ? __ldg(H + dir) : 0u;
-  double d0 = bwd ? __ldg(Dd) : 1.0, d1 = bwd && S > 1 ? __ldg(Dd - 32) : 1.0;
-  int m0 = pairs(h0);
-  int kp = bwd ? Kp - m0 : 0;  // first pair row of the current step
-  prefetch(kp);
-  tload<NP>(A, Lp, Cp, kp, m0, (h0 >> sh) & 0xff);
-  for (int s = 0; s < S; s += 2) {
-    // step s: A current, B <- step s + 1
-    const uint32_t h2 = s + 2 < S ? __ldg(H + 2 * dir) : 0u;
-    const double d2 = bwd && s + 2 < S ? __ldg(Dd - 64) : 1.0;
-    const int m1 = pairs(h1);
-    const int kp1 = bwd ? kp - m1 : kp + m0;
-    prefetch(kp);
-    if (s + 1 < S) tload<NP>(B, Lp, Cp, kp1, m1, (h1 >> sh) & 0xff);
-    {
-      const int node = h0 & 0xffff;
-      double a = tsm[X + node];
-      if (bwd) a = a / d0;
-      tsm[X + node] = tdot<NP>(A, m0, a, X);
+    const int mp = (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
+    H[t * 32 + lane] = (uint32_t)node | (cb << 8) | ((uint32_t)mp << 16);
+    Dd[t * 32 + lane] = dv;
+    for (int k = 0; k < 2 * mp; ++k) {
+      const bool in = k < (int)cb;
+      const long long ix = ((long long)(kp + k / 2) * 32 + lane) * 2 + (k & 1);
+      Lc[ix] = in ? bLv[b0 + k] : 0.0;
+      Ic[ix] = (uint8_t)(in ? bkv[b0 + k] : P.dummy);
     }
-    if (s + 1 >= S) break;
-    // step s + 1: B current, A <- step s + 2
-    const uint32_t h3 = s + 3 < S ? __ldg(H + 3 * dir) : 0u;
-    const double d3 = bwd && s + 3 < S ? __ldg(Dd - 96) : 1.0;
-    const int m2 = pairs(h2);
-    const int kp2 = bwd ? kp1 - m2 : kp1 + m1;
-    if (s + 2 < S) tload<NP>(A, Lp, Cp, kp2, m2, (h2 >> sh) & 0xff);
-    {
-      const int node = h1 & 0xffff;
-      double a = tsm[X + node];
-      if (bwd) a = a / d1;
-      tsm[X + node] = tdot<NP>(B, m1, a, X);
-    }
-    H += 2 * dir; Dd -= 64;
-    h0 = h2; h1 = h3; d0 = d2; d1 = d3; m0 = m2; kp = kp2;
+    kp += mp;
   }
 }
 
@@ -396,16 +167,311 @@ __device__ __forceinline__ TPatch tpatch(const PatchGeom& G, long long j) {
   return c;
 }
 
-// ------------------------------------------------------------------ middle phase
-// Lane = patch, no shared memory (high occupancy); the patch vectors are the
-// lane's columns of warp-interleaved global buffers [warp][node][32] (every access
-// of a warp is one 256-byte row).  x: pre-smoothed iterate, y: after the coarse
-// correction, s: residual handed to the post-smoothing.
-
-// Thread mode: coarse-level box bound per axis (tmode requires n_1 <= 32)
+// Level-1 (coarse) box of the thread kernel: at most CX x CX x CZ nodes.  The dense
+// V-cycle operator C of levels >= 1 (symmetric, reading c5) is stored as the upper
+// triangle of this fixed box, interleaved by warp slot: Cp[w][idx][32], idx over
+// (a <= b) row by row; coarse nodes a clipped boundary patch lacks have zero rows.
 template <int DIM> struct TCoarse {
   static constexpr int CX = DIM == 3 ? 3 : 5, CZ = DIM == 3 ? 3 : 1, NC = CX * CX * CZ;
+  static constexpr int NPK = NC * (NC + 1) / 2;
 };
+
+template <int DIM>
+__global__ void k_pack_c(const double* __restrict__ Cd, double* __restrict__ Cp, const int* __restrict__ pord,
+                         PatchGeom G, long long nslots, int ldc) {
+  constexpr int CX = TCoarse<DIM>::CX, NC = TCoarse<DIM>::NC, NPK = TCoarse<DIM>::NPK;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= nslots * NPK) return;
+  const int q = (int)(t % 32);
+  int idx = (int)((t / 32) % NPK);
+  const long long w = t / (32ll * NPK);
+  const long long j = pord[w * 32 + q];
+  double v = 0.0;
+  if (j >= 0) {
+    int a = 0;
+    while (idx >= NC - a) { idx -= NC - a; ++a; }
+    const int bb = a + idx;
+    const TPatch c = tpatch<DIM>(G, j);
+    const int ax = a % CX, ay = (a / CX) % CX, az = a / (CX * CX);
+    const int bx = bb % CX, by = (bb / CX) % CX, bz = bb / (CX * CX);
+    if (ax < c.cext[0] && ay < c.cext[1] && az < c.cext[2] && bx < c.cext[0] && by < c.cext[1] && bz < c.cext[2]) {
+      const int ia = ax + c.cext[0] * (ay + c.cext[1] * az), ib = bx + c.cext[0] * (by + c.cext[1] * bz);
+      v = Cd[j * ldc + (long long)ia * c.n1 + ib];
+    }
+  }
+  Cp[t] = v;
+}
+
+int trec_build(lorpc_prec* b, cudaStream_t s) {
+  const long long nw = (b->J + 31) / 32, nslots = nw * 32;
+  int TX = 32, TY = 8;
+  if (const char* e = getenv("LORPC_TILE")) {  // "0": lexicographic order; "TXxTY" otherwise
+    if (atoi(e) == 0) TX = TY = 1 << 30;
+    else sscanf(e, "%dx%d", &TX, &TY);
+  }
+  const std::vector<int> ord = tile_order(b, TX, TY);
+  LORPC_TRY(dalloc(&b->pord, ord.size()));
+  LORPC_CUDA(cudaMemcpyAsync(b->pord, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice, s));
+  TRecParams P{};
+  P.rec = b->rec; P.recoff = b->recoff; P.pord = b->pord; P.L = b->L; P.dummy = b->max_n[0];
+  long long* sizes = nullptr;
+  LORPC_TRY(dalloc(&sizes, (size_t)nw));
+  P.sizes = sizes;
+  const unsigned blocks = (unsigned)((nslots + 127) / 128);
+  k_trec<<<blocks, 128, 0, s>>>(P, nslots, 0);
+  LORPC_LAUNCHED();
+  std::vector<long long> h((size_t)nw);
+  LORPC_CUDA(cudaMemcpyAsync(h.data(), sizes, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  long long off = 0;
+  for (auto& v : h) { const long long sz = v; v = off; off += sz; }
+  b->trec_bytes = off;
+  LORPC_TRY(dalloc(&b->trec, (size_t)off));
+  LORPC_TRY(dalloc(&b->trecoff, h.size()));
+  LORPC_CUDA(cudaMemcpyAsync(b->trecoff, h.data(), sizeof(long long) * h.size(), cudaMemcpyHostToDevice, s));
+  P.trec = b->trec; P.trecoff = b->trecoff;
+  k_trec<<<blocks, 128, 0, s>>>(P, nslots, 1);
+  LORPC_LAUNCHED();
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  dfree(sizes);
+  // packed dense coarse operators; park buffers x, y, s
+  const PatchGeom G = make_geom(b);
+  const int npk = b->m->d == 3 ? TCoarse<3>::NPK : TCoarse<2>::NPK;
+  LORPC_TRY(dalloc(&b->Cdi, (size_t)(nslots * npk)));
+  if (b->m->d == 3) k_pack_c<3><<<nb(nslots * npk, 256), 256, 0, s>>>(b->Cd, b->Cdi, b->pord, G, nslots, b->ldc);
+  else k_pack_c<2><<<nb(nslots * npk, 256), 256, 0, s>>>(b->Cd, b->Cdi, b->pord, G, nslots, b->ldc);
+  LORPC_LAUNCHED();
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  dfree(b->Cd);
+  LORPC_TRY(dalloc(&b->zpark, (size_t)(nslots * 3 * b->max_n[0])));
+  return LORPC_OK;
+}
+
+// ------------------------------------------------------------------ kernel
+extern __shared__ __align__(16) double tsm[];
+
+struct TcParams {
+  PatchGeom G;
+  const double* A0;  // finest LOR level, node-major rows of NDP doubles
+  const double* W;   // separable restriction tables, level 0 -> 1
+  int woff[4];
+  const char* trec;
+  const long long* trecoff;
+  const int* pord;
+  long long J, nslots;
+  const double* Cp;  // [warps][NPK][32] packed dense coarse operators
+  double *xpark, *ypark, *spark;  // [warp][n0max][32] x, y, s of the warp's patches (lane columns)
+  int n0max;         // largest finest-level patch (= the dummy node index)
+  int tpoff;         // the warp's 32 patch geometries (TPatch)
+  int pfd;           // L2 prefetch distance of the sweeps (pair rows)
+  int warp_doubles;
+  const double* r;
+  double* z;
+};
+
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Shared-memory layout of the warp's 32 patch vectors: node i of patch (lane) q
+// at word 33 i + q, conflict-free for lanes = patches at one node and for lanes =
+// consecutive nodes of one patch.  X points at the lane's column (word q).
+#define VO(i, q) ((i) * 33 + (q))
+
+// One sweep step's column data, register-resident (NP = max pairs per column)
+template <int NP>
+struct TStage {
+  double2 l[NP];
+  uint32_t c[NP];
+};
+// Loads of one step: mp pair rows (warp-uniform) from pair row kp.  Lanes whose
+// column is shorter skip the value loads of their padding pairs (no memory
+// traffic); stale register values there meet the dummy node (see tfwd / tbwd), so
+// the stage starts finite (zeroed).  The node indices are always loaded (padding
+// holds the dummy).  Entered by a jump into a fall-through sequence.
+#define LORPC_TL_PAIR(P_)                                            \
+  if ((P_) < NP) {                                                   \
+    constexpr int pp = (P_) < NP ? (P_) : 0;                         \
+    if (2 * pp < cnt) s.l[pp] = __ldcs(Lq + pp * 32);                \
+    s.c[pp] = __ldcs(Cq + pp * 32);                                  \
+  }
+template <int NP>
+__device__ __forceinline__ void tload(TStage<NP>& s, const double2* __restrict__ Lp, const uint16_t* __restrict__ Cp,
+                                      int kp, int mp, int cnt) {
+  const double2* Lq = Lp + (long long)kp * 32;
+  const uint16_t* Cq = Cp + (long long)kp * 32;
+  switch (mp) {
+    case 13: LORPC_TL_PAIR(12); [[fallthrough]];
+    case 12: LORPC_TL_PAIR(11); [[fallthrough]];
+    case 11: LORPC_TL_PAIR(10); [[fallthrough]];
+    case 10: LORPC_TL_PAIR(9); [[fallthrough]];
+    case 9: LORPC_TL_PAIR(8); [[fallthrough]];
+    case 8: LORPC_TL_PAIR(7); [[fallthrough]];
+    case 7: LORPC_TL_PAIR(6); [[fallthrough]];
+    case 6: LORPC_TL_PAIR(5); [[fallthrough]];
+    case 5: LORPC_TL_PAIR(4); [[fallthrough]];
+    case 4: LORPC_TL_PAIR(3); [[fallthrough]];
+    case 3: LORPC_TL_PAIR(2); [[fallthrough]];
+    case 2: LORPC_TL_PAIR(1); [[fallthrough]];
+    case 1: LORPC_TL_PAIR(0); [[fallthrough]];
+    default: break;
+  }
+}
+#undef LORPC_TL_PAIR
+
+// forward (push) step: yk = X[k]; X[i] -= L_ik yk for the column; X[k] = yk / D_k.
+// All neighbour values are loaded before any is stored (the column's nodes are
+// distinct, padding aside), so the loads issue back to back.
+#define LORPC_FL(P_)                                                      \
+  if ((P_) < NP) {                                                        \
+    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
+    v0[pp] = X[33 * (s.c[pp] & 0xff)];                                    \
+    v1[pp] = X[33 * (s.c[pp] >> 8)];                                      \
+  }
+#define LORPC_FS(P_)                                                      \
+  if ((P_) < NP) {                                                        \
+    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
+    X[33 * (s.c[pp] & 0xff)] = v0[pp] - s.l[pp].x * yk;                   \
+    X[33 * (s.c[pp] >> 8)] = v1[pp] - s.l[pp].y * yk;                     \
+  }
+#define LORPC_CASES(M_)                                                   \
+  switch (mp) {                                                           \
+    case 13: M_(12); [[fallthrough]];                                     \
+    case 12: M_(11); [[fallthrough]];                                     \
+    case 11: M_(10); [[fallthrough]];                                     \
+    case 10: M_(9); [[fallthrough]];                                      \
+    case 9: M_(8); [[fallthrough]];                                       \
+    case 8: M_(7); [[fallthrough]];                                       \
+    case 7: M_(6); [[fallthrough]];                                       \
+    case 6: M_(5); [[fallthrough]];                                       \
+    case 5: M_(4); [[fallthrough]];                                       \
+    case 4: M_(3); [[fallthrough]];                                       \
+    case 3: M_(2); [[fallthrough]];                                       \
+    case 2: M_(1); [[fallthrough]];                                       \
+    case 1: M_(0); [[fallthrough]];                                       \
+    default: break;                                                       \
+  }
+template <int NP>
+__device__ __forceinline__ void tfwd_step(const TStage<NP>& s, int mp, uint32_t h, double dinv, double* X) {
+  const int k = h & 0xff;
+  const double yk = X[33 * k];
+  double v0[NP], v1[NP];
+  LORPC_CASES(LORPC_FL)
+  LORPC_CASES(LORPC_FS)
+  X[33 * k] = yk * dinv;
+}
+// backward (pull) step: X[k] -= sum_i L_ik X[i]; four partial sums
+#define LORPC_BD(P_)                                                      \
+  if ((P_) < NP) {                                                        \
+    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
+    a[2 * (pp & 1)] -= s.l[pp].x * X[33 * (s.c[pp] & 0xff)];              \
+    a[2 * (pp & 1) + 1] -= s.l[pp].y * X[33 * (s.c[pp] >> 8)];            \
+  }
+template <int NP>
+__device__ __forceinline__ void tbwd_step(const TStage<NP>& s, int mp, uint32_t h, double* X) {
+  const int k = h & 0xff;
+  double a[4] = {X[33 * k], 0.0, 0.0, 0.0};
+  LORPC_CASES(LORPC_BD)
+  X[33 * k] = (a[0] + a[1]) + (a[2] + a[3]);
+}
+#undef LORPC_FL
+#undef LORPC_FS
+#undef LORPC_BD
+
+// One triangular sweep of the lane's own patch over the T-record block: forward
+// (push, steps ascending, diagonal fused) or backward (pull, steps descending).
+// Software-pipelined one step deep (unrolled by two so that the register stages
+// swap roles without moves): the next step's column is loaded while the current
+// one is applied, and the record streams through L2 prefetches TPFD pair rows
+// ahead.  X = the lane's column of the warp's shared vectors; X[33 * dummy] must be
+// zero on entry to the backward sweep (padding entries read it).
+template <int NP, bool BWD>
+__device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
+  const int4 hd = __ldg((const int4*)blk);
+  const int S = hd.x, Kp = hd.y;
+  if (S == 0) return;
+  const TRecLayout T = trec_layout(S, Kp);
+  const int dir = BWD ? -32 : 32;
+  const uint32_t* H = (const uint32_t*)(blk + T.hdr) + lane + (BWD ? (S - 1) * 32 : 0);
+  const double* Dd = (const double*)(blk + T.D) + lane;
+  const double2* Lp = (const double2*)(blk + T.Lc) + lane;
+  const uint16_t* Cp = (const uint16_t*)(blk + T.Ic) + lane;
+  // L2 prefetch cursor (pair rows; forward ascending, backward descending)
+  int pf = 0;
+  auto prefetch = [&](int kp) {
+    if (lane != 0) return;
+    if (!BWD) {
+      while (pf < Kp && pf < kp + TPFD) {
+        const int nr = min(8, Kp - pf);
+        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
+        l2_prefetch(Cp - lane + pf * 32, 64u * nr);
+        pf += nr;
+      }
+    } else {
+      while (pf > 0 && pf > kp - TPFD) {
+        const int nr = min(8, pf);
+        pf -= nr;
+        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
+        l2_prefetch(Cp - lane + pf * 32, 64u * nr);
+      }
+    }
+  };
+  if (lane == 0) {
+    l2_prefetch((const uint32_t*)(blk + T.hdr), 128u * S);
+    if (!BWD) l2_prefetch((const double*)(blk + T.D), 256u * S);
+    pf = BWD ? Kp : 0;
+  }
+  auto mpof = [](uint32_t h) { return (int)((h >> 16) & 0xffu); };
+  auto cntof = [](uint32_t h) { return (int)((h >> 8) & 0xffu); };
+  TStage<NP> A, B;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { A.l[p] = B.l[p] = make_double2(0.0, 0.0); A.c[p] = B.c[p] = 0u; }
+  const int t0 = BWD ? S - 1 : 0;
+  uint32_t h0 = __ldg(H), h1 = S > 1 ? __ldg(H + dir) : 0u;
+  double d0 = BWD ? 1.0 : __ldg(Dd + 32 * t0), d1 = !BWD && S > 1 ? __ldg(Dd + 32) : 1.0;
+  int m0 = mpof(h0);
+  int kp = BWD ? Kp - m0 : 0;  // first pair row of the current step
+  prefetch(kp);
+  tload<NP>(A, Lp, Cp, kp, m0, cntof(h0));
+  for (int s = 0; s < S; s += 2) {
+    // step s: A current, B <- step s + 1
+    const uint32_t h2 = s + 2 < S ? __ldg(H + 2 * dir) : 0u;
+    const double d2 = !BWD && s + 2 < S ? __ldg(Dd + 32 * (s + 2)) : 1.0;
+    const int m1 = mpof(h1);
+    const int kp1 = BWD ? kp - m1 : kp + m0;
+    prefetch(kp);
+    if (s + 1 < S) tload<NP>(B, Lp, Cp, kp1, m1, cntof(h1));
+    if (BWD) tbwd_step<NP>(A, m0, h0, X); else tfwd_step<NP>(A, m0, h0, d0, X);
+    if (s + 1 >= S) break;
+    // step s + 1: B current, A <- step s + 2
+    const uint32_t h3 = s + 3 < S ? __ldg(H + 3 * dir) : 0u;
+    const double d3 = !BWD && s + 3 < S ? __ldg(Dd + 32 * (s + 3)) : 1.0;
+    const int m2 = mpof(h2);
+    const int kp2 = BWD ? kp1 - m2 : kp1 + m1;
+    if (s + 2 < S) tload<NP>(A, Lp, Cp, kp2, m2, cntof(h2));
+    if (BWD) tbwd_step<NP>(B, m1, h1, X); else tfwd_step<NP>(B, m1, h1, d1, X);
+    H += 2 * dir;
+    h0 = h2; h1 = h3; d0 = d2; d1 = d3; m0 = m2; kp = kp2;
+  }
+}
+
+// M^{-1} applied in place to the lane's column X (forward, dummy reset, backward)
+template <int NP>
+__device__ __forceinline__ void tsmooth(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
+  tsweep<NP, false>(blk, X, TPFD, lane);
+  X[33 * dummy] = 0.0;
+  tsweep<NP, true>(blk, X, TPFD, lane);
+}
+
+// ------------------------------------------------------------------ middle phase
+// Lane = patch, no shared memory; the patch vectors are the lane's columns of
+// warp-interleaved global buffers [warp][node][32] (every access of a warp is one
+// 256-byte row).  x: pre-smoothed iterate, y: after the coarse correction, s:
+// residual handed to the post-smoothing.  The lanes of a warp walk their nodes in
+// lock step; the walk runs down in z (and y) on patches of odd z (y) index, so a
+// patch and its z- (y-) neighbour, one tile layer (row) apart and resident at the
+// same time, read the LOR rows of their shared node planes at the same point of
+// the walk, and the second read hits L2.
 
 // 1D restriction weights of fine node (ix, iy, iz) to the coarse box (dense W[c][f],
 // zero off the hat support)
@@ -451,16 +517,40 @@ __device__ __forceinline__ double tres_node(const TcParams& P, const TPatch& c, 
   return a0 + a1;
 }
 
+// node of walk step k: box coordinates with y / z reversed on odd patch rows / layers
+struct TWalk {
+  int ex, ey, ez, fy, fz;
+  float rex, rexy;
+  __device__ __forceinline__ int at(int k, int& ix, int& iy, int& iz) const {
+    box_xyz(k, ex, ey, rex, rexy, ix, iy, iz);
+    if (fy) iy = ey - 1 - iy;
+    if (fz) iz = ez - 1 - iz;
+    return ix + ex * (iy + ey * iz);
+  }
+};
+template <int DIM>
+__device__ __forceinline__ TWalk twalk(const PatchGeom& G, const TPatch& c, long long j) {
+  TWalk t;
+  t.ex = c.ext[0]; t.ey = c.ext[1]; t.ez = c.ext[2];
+  t.rex = 1.0f / c.ext[0]; t.rexy = 1.0f / (c.ext[0] * c.ext[1]);
+  const long long gx = G.kind == 0 ? G.n[0] + 1 : G.n[0], gy = G.kind == 0 ? G.n[1] + 1 : G.n[1];
+  t.fy = (int)((j / gx) % gy) & 1;
+  t.fz = DIM == 3 ? (int)(j / (gx * gy)) & 1 : 0;
+  return t;
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
-  constexpr int CX = TCoarse<DIM>::CX, CZ = TCoarse<DIM>::CZ, NC = TCoarse<DIM>::NC, NC1 = 32;
-  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long w = j >> 5;
+  constexpr int CX = TCoarse<DIM>::CX, CZ = TCoarse<DIM>::CZ, NC = TCoarse<DIM>::NC, NPK = TCoarse<DIM>::NPK;
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (slot >= P.nslots) return;
+  const long long j = P.pord[slot];
+  if (j < 0) return;
+  const long long w = slot >> 5;
   const int lane = threadIdx.x & 31;
-  if (j >= P.J) return;
   const TPatch c = tpatch<DIM>(P.G, j);
-  const int n0 = P.n0max, ex = c.ext[0], ey = c.ext[1];
-  const float rex = 1.0f / ex, rexy = 1.0f / (ex * ey);
+  const TWalk wk = twalk<DIM>(P.G, c, j);
+  const int n0 = P.n0max;
   const long long col = w * (long long)n0 * 32 + lane;
   const double* Xp = P.xpark + col;
   double* Yp = P.ypark + col;
@@ -469,9 +559,9 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
   double r1[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) r1[k] = 0.0;
-  for (int f = 0; f < c.n; ++f) {
+  for (int k = 0; k < c.n; ++k) {
     int ix, iy, iz;
-    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    const int f = wk.at(k, ix, iy, iz);
     const double sv = tres_node<DIM>(P, c, Xp, f, ix, iy, iz);
     double wx[CX], wy[CX], wz[CZ];
     tweights<DIM>(P, c, ix, iy, iz, wx, wy, wz);
@@ -484,45 +574,28 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
         for (int kx = 0; kx < CX; ++kx) r1[kx + CX * (ky + CX * kz)] += wx[kx] * wv;
       }
   }
-  // z_1 = C r_1: r_1 to the patch's coarse numbering, C interleaved by lane
-  const int n1 = c.n1, cx = c.cext[0], cy = c.cext[1], cz = c.cext[2];
-  double* R = P.rz + w * 2ll * P.n1max * 32 + lane;
-  double* Z = R + P.n1max * 32;
-#pragma unroll
-  for (int kz = 0; kz < CZ; ++kz)
-#pragma unroll
-    for (int ky = 0; ky < CX; ++ky)
-#pragma unroll
-      for (int kx = 0; kx < CX; ++kx)
-        if (kx < cx && ky < cy && kz < cz) R[(kx + cx * (ky + cy * kz)) * 32] = r1[kx + CX * (ky + CX * kz)];
-  {
-    const double* C = P.Cd + w * 32ll * P.ldc + lane;
-    double zc[NC1];
-#pragma unroll
-    for (int i = 0; i < NC1; ++i) zc[i] = 0.0;
-    for (int k = 0; k < n1; ++k) {
-      const double rk = R[k * 32];
-      const double* Ck = C + (long long)k * n1 * 32;
-#pragma unroll
-      for (int i = 0; i < NC1; ++i)
-        if (i < n1) zc[i] += __ldcs(Ck + i * 32) * rk;
-    }
-#pragma unroll
-    for (int i = 0; i < NC1; ++i)
-      if (i < n1) Z[i * 32] = zc[i];
-  }
-  // y = x + P z_1
+  // z_1 = C r_1 (packed symmetric, fixed coarse box, interleaved by lane)
   double z1[NC];
 #pragma unroll
-  for (int kz = 0; kz < CZ; ++kz)
+  for (int k = 0; k < NC; ++k) z1[k] = 0.0;
+  {
+    const double* C = P.Cp + w * 32ll * NPK + lane;
+    int idx = 0;
 #pragma unroll
-    for (int ky = 0; ky < CX; ++ky)
+    for (int a = 0; a < NC; ++a) {
 #pragma unroll
-      for (int kx = 0; kx < CX; ++kx)
-        z1[kx + CX * (ky + CX * kz)] = (kx < cx && ky < cy && kz < cz) ? Z[(kx + cx * (ky + cy * kz)) * 32] : 0.0;
-  for (int f = 0; f < c.n; ++f) {
+      for (int b = a; b < NC; ++b) {
+        const double cv = __ldcs(C + 32 * idx);
+        z1[a] += cv * r1[b];
+        if (b != a) z1[b] += cv * r1[a];
+        ++idx;
+      }
+    }
+  }
+  // y = x + P z_1
+  for (int k = 0; k < c.n; ++k) {
     int ix, iy, iz;
-    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    const int f = wk.at(k, ix, iy, iz);
     double wx[CX], wy[CX], wz[CZ];
     tweights<DIM>(P, c, ix, iy, iz, wx, wy, wz);
     double t = 0.0;
@@ -538,9 +611,9 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
     Yp[f * 32] = Xp[f * 32] + t;
   }
   // s = r - A y
-  for (int f = 0; f < c.n; ++f) {
+  for (int k = 0; k < c.n; ++k) {
     int ix, iy, iz;
-    box_xyz(f, ex, ey, rex, rexy, ix, iy, iz);
+    const int f = wk.at(k, ix, iy, iz);
     __stcs(Sp + f * 32, tres_node<DIM>(P, c, Yp, f, ix, iy, iz));
   }
 }
@@ -553,12 +626,12 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   constexpr int NP = DIM == 3 ? 13 : 4;
   const int lane = threadIdx.x;
   const long long w = blockIdx.x;
-  const int X = 0, n0 = P.n0max;
+  const int n0 = P.n0max;
   const int nq = (int)min(32ll, P.J - w * 32);
   const char* blk = P.trec + P.trecoff[w];
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
   TPatch* tpa = (TPatch*)(tsm + P.tpoff);
-  if (lane < nq) tpa[lane] = tpatch<DIM>(P.G, w * 32 + lane);
+  if (lane < nq) tpa[lane] = tpatch<DIM>(P.G, P.pord[w * 32 + lane]);
   const long long col = w * (long long)n0 * 32 + lane;
   if (!POST) {
     __syncwarp();
@@ -568,20 +641,20 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
       for (int i = lane; i < c.n; i += 32) {
         int ix, iy, iz;
         box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
-        tsm[X + VO(i, q)] = __ldg(P.r + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
+        tsm[VO(i, q)] = __ldg(P.r + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
       }
     }
   } else {
-    for (int i = 0; i < n0; ++i) tsm[X + VO(i, lane)] = __ldcs(P.spark + col + i * 32);
+    for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] = __ldcs(P.spark + col + i * 32);
   }
-  tsm[X + VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
+  tsm[VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
-#pragma unroll 1
-  for (int sw = 0; sw < 2; ++sw) tsweep<NP>(blk, X, n0, sw == 1, P.pfd, lane);
+  tsmooth<NP>(blk, tsm + lane, n0, P.pfd, lane);
+  __syncwarp();
   if (!POST) {
-    for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[X + VO(i, lane)]);
+    for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[VO(i, lane)]);
   } else {
-    for (int i = 0; i < n0; ++i) tsm[X + VO(i, lane)] += __ldcs(P.ypark + col + i * 32);
+    for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] += __ldcs(P.ypark + col + i * 32);  // z_j = y + M^{-1} s
     __syncwarp();
     for (int q = 0; q < nq; ++q) {  // z += I_j z_j (a8), lanes over consecutive nodes
       const TPatch c = tpa[q];
@@ -590,7 +663,7 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
         int ix, iy, iz;
         box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
         atomicAdd(P.z + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)),
-                  tsm[X + VO(i, q)]);
+                  tsm[VO(i, q)]);
       }
     }
   }
@@ -602,11 +675,12 @@ static TcParams make_tparams(const lorpc_prec* b, const double* r, double* z) {
   P.A0 = b->lor->A[0];
   P.W = b->wtab;
   memcpy(P.woff, b->woff[0], sizeof(P.woff));
-  P.trec = b->trec; P.trecoff = b->trecoff; P.J = b->J;
-  P.Cd = b->Cdi; P.ldc = b->ldc;
-  P.n0max = b->max_n[0]; P.n1max = b->max_n[1];
-  const long long nw = (b->J + 31) / 32, pcol = nw * b->max_n[0] * 32;
-  P.xpark = b->zpark; P.ypark = b->zpark + pcol; P.spark = b->zpark + 2 * pcol; P.rz = b->zpark + 3 * pcol;
+  P.trec = b->trec; P.trecoff = b->trecoff; P.pord = b->pord;
+  P.J = b->J; P.nslots = (b->J + 31) / 32 * 32;
+  P.Cp = b->Cdi;
+  P.n0max = b->max_n[0];
+  const long long pcol = P.nslots * b->max_n[0];
+  P.xpark = b->zpark; P.ypark = b->zpark + pcol; P.spark = b->zpark + 2 * pcol;
   P.r = r; P.z = z;
   int acc = VO(b->max_n[0] + 1, 0);
   P.tpoff = acc; acc += 32 * (int)(sizeof(TPatch) / sizeof(double));
@@ -621,9 +695,14 @@ size_t tmode_smem(const lorpc_prec* b) {
 
 int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
   const TcParams P = make_tparams(b, r, z);
-  const size_t smem = (size_t)P.warp_doubles * sizeof(double);
+  size_t smem = (size_t)P.warp_doubles * sizeof(double);
+  // optional occupancy cap of the smoothing kernels (warps per SM), for L2 reuse studies
+  if (const char* e = getenv("LORPC_SMOOTH_WPSM")) {
+    const int wpsm = atoi(e);
+    if (wpsm > 0) smem = std::max(smem, (size_t)(220 * 1024 / wpsm));
+  }
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
-  const unsigned wblocks = (unsigned)((b->J + 31) / 32), mblocks = (unsigned)((b->J + 127) / 128);
+  const unsigned wblocks = (unsigned)(P.nslots / 32), mblocks = (unsigned)((P.nslots + 127) / 128);
   if (b->m->d == 2) {
     cudaFuncSetAttribute(k_vt_smooth<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_vt_smooth<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
