@@ -491,6 +491,13 @@ __device__ __forceinline__ void tweights(const TcParams& P, const TPatch& c, int
   for (int k = 0; k < CZ; ++k) wz[k] = DIM == 3 ? (k < c.cext[2] ? __ldg(Wz + k * c.ext[2] + iz) : 0.0) : 1.0;
 }
 
+// one 256-bit load (LDG.E.ENL2.256): a lane-per-patch walk reads a different row in
+// every lane, so each warp load costs one L1 wavefront per lane; four doubles per
+// load halve the wavefronts of 16-byte loads
+__device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 // s_i = r_i - (A_0 v)_i at node i of the lane's patch, v = the lane's column V
 template <int DIM>
 __device__ __forceinline__ double tres_node(const TcParams& P, const TPatch& c, const double* __restrict__ V, int i,
@@ -501,17 +508,33 @@ __device__ __forceinline__ double tres_node(const TcParams& P, const TPatch& c, 
   const unsigned gi = (unsigned)((c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
   const uint32_t em = exist_mask<DIM>(ix, iy, iz, ex, ey, ez);
   double a0 = __ldg(P.r + gi), a1 = 0.0;
-  const double2* Ar = (const double2*)(P.A0 + (size_t)gi * NDP);
+  const double* Ar = P.A0 + (size_t)gi * NDP;
+  if constexpr (NDP % 4 == 0) {
 #pragma unroll
-  for (int d2 = 0; d2 < NDP / 2; ++d2) {
-    const double2 av = __ldg(Ar + d2);
+    for (int d4 = 0; d4 < NDP / 4; ++d4) {
+      double av[4];
+      ld256(Ar + 4 * d4, av[0], av[1], av[2], av[3]);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int d = 2 * d2 + h;
-      if (d >= ND) break;
-      const int o = dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
-      const double v = (em & (1u << d)) ? V[(i + o) * 32] : 0.0;
-      if (h) a1 -= av.y * v; else a0 -= av.x * v;
+      for (int h = 0; h < 4; ++h) {
+        const int d = 4 * d4 + h;
+        if (d >= ND) break;
+        const int o = dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
+        const double v = (em & (1u << d)) ? V[(i + o) * 32] : 0.0;
+        if (h & 1) a1 -= av[h] * v; else a0 -= av[h] * v;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int d2 = 0; d2 < NDP / 2; ++d2) {
+      const double2 av = __ldg((const double2*)Ar + d2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int d = 2 * d2 + h;
+        if (d >= ND) break;
+        const int o = dir_dx(d) + ex * (dir_dy(d) + ey * (DIM == 3 ? dir_dz(d) : 0));
+        const double v = (em & (1u << d)) ? V[(i + o) * 32] : 0.0;
+        if (h) a1 -= av.y * v; else a0 -= av.x * v;
+      }
     }
   }
   return a0 + a1;
