@@ -159,6 +159,59 @@ int lorpc_pcg_solve(const lorpc_mesh* m, const lorpc_prec* b, const double* b_de
 int lorpc_pcg_solve_host(const lorpc_mesh* m, const lorpc_prec* b, const double* b_host, double* x_host,
                          double rtol, int maxit, lorpc_pcg_report* rep, void* stream);
 
+/* ---- multi-GPU slab decomposition (BASELINE C5 "element slabs
+ * partitioned across 1/2/4/8 GPUs with NCCL halo exchange") ------------------ */
+/* 3D CG only.  Rank r of R owns element layers [z0, z1) along z (balanced:
+ * z0 = floor(n_z r / R)), node planes [z0 p, z1 p) and vertex planes [z0, z1)
+ * (the last rank also the top plane): its owned nodes are one contiguous range
+ * of the global node vector (z is the slowest axis).  It builds a local sub-mesh
+ * of element layers [za, zb) = [z0 - 1, z1 + 1] clipped to the domain from the
+ * replicated vertex array (one ghost layer per side), so LOR rows, patch factors
+ * (vertex patches of its owned vertex planes, eq:patch P:302-315) and coarse rows
+ * are computed locally; R_0 (reading c11) runs replicated on the gathered global
+ * vertex-level operator.  Per PCG iteration four point-to-point exchanges
+ * (phases below), one allreduce of the coarse residual on the vertex grid and
+ * the scalar allreduces. */
+typedef struct {
+  int z0, z1, za, zb;          /* owned / local element layers (global indices) */
+  int own_plane0, own_planes;  /* owned node planes: local index of the first, count */
+  int gown_plane0;             /* global index of the first owned node plane */
+  int vown0, nvown;            /* owned vertex planes: local index of the first, count */
+  /* phase k: 0 = operator input (copy), 1 = operator output partial sums (add on
+   * free nodes), 2 = Schwarz input r halo (copy), 3 = Schwarz output patch sums
+   * (add).  Send nplanes[k] planes from local plane send0[k] to rank to[k];
+   * receive nplanes[k] planes into local plane recv0[k] from rank from[k]; -1 =
+   * none. */
+  int to[4], from[4], send0[4], recv0[4], nplanes[4];
+} lorpc_dist_plan;
+typedef struct lorpc_dist lorpc_dist;
+/* The slab plan of rank `rank` (host only, no device work): LORPC_ERR_ARG unless
+ * n_z >= nranks >= 1 and p >= 1. */
+int lorpc_dist_plan_get(int n_z, int p, int nranks, int rank, lorpc_dist_plan* out);
+/* ncclGetUniqueId (128 bytes) — called on rank 0, broadcast by the caller. */
+int lorpc_dist_nccl_id(void* id128);
+/* Builds the rank's local problem.  desc / vertices_host describe the GLOBAL
+ * mesh.  nccl_id != NULL: one rank per process (device = current device),
+ * NCCL communicator of nranks ranks (collective call).  nccl_id == NULL:
+ * emulation — all nranks ranks in this process on the current device, the
+ * exchanges done by device copies (testing the multi-rank path on one GPU).
+ * sdesc must request vertex patches with the GMG coarse term.  Synchronizes. */
+int lorpc_dist_create(const lorpc_mesh_desc* desc, const double* vertices_host, const lorpc_schwarz_desc* sdesc,
+                      int nranks, int rank, const void* nccl_id, void* stream, lorpc_dist** out);
+void lorpc_dist_destroy(lorpc_dist* d);
+/* Local rank `local` (0 in NCCL mode; 0..nranks-1 in emulation): global index of
+ * its first owned node, owned node count, patch count. */
+int lorpc_dist_info(const lorpc_dist* d, int local, long long* owned_offset, long long* n_owned, long long* n_patches);
+/* y = A x and z = B r on the distributed vectors: arrays of one device pointer per
+ * local rank, each the rank's owned range [owned_offset, owned_offset + n_owned)
+ * of the global vector.  Asynchronous on the creation stream. */
+int lorpc_dist_operator_apply(lorpc_dist* d, const double* const* x_owned, double* const* y_owned);
+int lorpc_dist_precond_apply(lorpc_dist* d, const double* const* r_owned, double* const* z_owned);
+/* PCG (as lorpc_pcg_solve) on the distributed vectors; dot products are global
+ * (fixed order per rank, then summed over ranks).  Synchronizes. */
+int lorpc_dist_pcg_solve(lorpc_dist* d, const double* const* b_owned, double* const* x_owned, double rtol,
+                         int maxit, lorpc_pcg_report* rep);
+
 /* Number of kernel launches issued by this library on the calling thread since
  * the last reset (instrumentation for the bench's gpu_launches claim). */
 long long lorpc_launch_count(int reset);

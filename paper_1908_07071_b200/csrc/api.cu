@@ -78,6 +78,7 @@ int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, 
     if (k < d) { m->nloc *= m->p + 1; m->nq *= m->q; nvert *= m->n[k] + 1; }
   }
   m->ndof = desc->disc == 0 ? m->ndof_cg : m->nel * m->nloc;
+  m->ez_lo = 0; m->ez_hi = m->n[2];
   m->nquad = m->nel * m->nq;
   m->nbq = 0;
   if (desc->disc != 0) {

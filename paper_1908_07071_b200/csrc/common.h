@@ -80,6 +80,7 @@ struct lorpc_mesh {
   int d, p, q, nloc, nq;            // nq = q^d
   int n[3], N[3];                   // elements / GLL nodes per axis (1 in unused axis)
   long long nel, ndof_cg, ndof, nquad, nbq;
+  int ez_lo = 0, ez_hi = 0;         // CG operator: element layers [ez_lo, ez_hi) along z (3D slabs; all by default)
   lorpc::Basis1D basis;
   double* V = nullptr;              // [nvert][d]
   double* G = nullptr;              // [nel][ncomp][nq] geometric factors
@@ -104,6 +105,7 @@ struct lorpc_prec {
   const lorpc_mesh* m;
   lorpc_schwarz_desc desc;
   long long J;                      // patches
+  int pvz0 = 0, pnvz = 0;           // vertex patches: planes [pvz0, pvz0 + pnvz) (0 = all; slab subsets)
   int L;
   int max_n[lorpc::MAXL];           // largest patch size per level
   char* rec = nullptr;              // per patch-level ILU records
@@ -167,6 +169,10 @@ int dg_restrict_cg(const lorpc_mesh* m, const double* r_dg, double* r_cg, cudaSt
 int dg_combine(const lorpc_mesh* m, const double* r_dg, const double* z_cg, double* z_dg, cudaStream_t s);
 int lor_build(const lorpc_mesh* m, lorpc_lor* l, cudaStream_t s);
 int schwarz_build(lorpc_prec* b, cudaStream_t s);
+int gmg_build(lorpc_prec* b, double* Ac0, const int* nv, int d, cudaStream_t s);
+int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
+int gmg_vcycle(const lorpc_prec* b, const double** out, cudaStream_t s);
+int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStream_t s);
 int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
 int quad_points(const lorpc_mesh* m, double* xq, double* xbq, cudaStream_t s);
 int rhs_assemble(const lorpc_mesh* m, const double* fq, const double* gq, double* b, cudaStream_t s);

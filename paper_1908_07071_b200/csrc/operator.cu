@@ -25,16 +25,15 @@ __global__ void k_pre(const double* __restrict__ x, double* __restrict__ y, int3
 template <int P, int EB>
 __global__ void __launch_bounds__((P + 1) * (P + 1) * EB)
 k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ G, int3 n, int3 N,
-      Basis1D bs) {
+      Basis1D bs, long long e0, long long e1) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q * Q * Q;
   __shared__ double sB[Q2], sD[Q2];
   __shared__ double S[EB][3][Q3];
   const int tx = threadIdx.x, ty = threadIdx.y, te = threadIdx.z;
   const int lt = tx + Q * (ty + Q * te);
   for (int i = lt; i < Q2; i += Q2 * EB) { sB[i] = bs.B[i]; sD[i] = bs.D[i]; }
-  const long long nel = (long long)n.x * n.y * n.z;
-  const long long e = (long long)blockIdx.x * EB + te;
-  const bool active = e < nel;
+  const long long e = e0 + (long long)blockIdx.x * EB + te;  // elements [e0, e1) (slab layers)
+  const bool active = e < e1;
   int ex = 0, ey = 0, ez = 0;
   if (active) { ex = (int)(e % n.x); ey = (int)((e / n.x) % n.y); ez = (int)(e / ((long long)n.x * n.y)); }
   const int gx = ex * P + tx, gy = ey * P + ty;
@@ -208,8 +207,10 @@ static void launch3(const lorpc_mesh* m, const double* x, double* y, cudaStream_
   int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   dim3 blk(Q, Q, EB);
-  unsigned grid = (unsigned)((m->nel + EB - 1) / EB);
-  k_cg3<P, EB><<<grid, blk, 0, s>>>(x, y, m->G, n, N, m->basis);
+  const long long e0 = (long long)m->ez_lo * m->n[0] * m->n[1], e1 = (long long)m->ez_hi * m->n[0] * m->n[1];
+  unsigned grid = (unsigned)((e1 - e0 + EB - 1) / EB);
+  if (grid == 0) return;
+  k_cg3<P, EB><<<grid, blk, 0, s>>>(x, y, m->G, n, N, m->basis, e0, e1);
 }
 template <int P>
 static void launch2(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {

@@ -12,12 +12,13 @@ struct PatchGeom {
   int ml[MAXL];         // nodes per element per axis at each level
   int Nax[MAXL][3];     // level grid per axis
   int L;
+  int vz0;              // vertex patches: z index of the first patch plane (slab subsets)
 };
 
 __host__ __device__ __forceinline__ void patch_elems(const PatchGeom& G, long long j, int* elo, int* ehi) {
   if (G.kind == 0) {
     const long long nv0 = G.n[0] + 1, nv1 = G.n[1] + 1;
-    const int v[3] = {(int)(j % nv0), (int)((j / nv0) % nv1), (int)(j / (nv0 * nv1))};
+    const int v[3] = {(int)(j % nv0), (int)((j / nv0) % nv1), (int)(j / (nv0 * nv1)) + G.vz0};
     for (int k = 0; k < 3; ++k) {
       if (k >= G.d) { elo[k] = ehi[k] = 0; continue; }
       elo[k] = v[k] - 1 < 0 ? 0 : v[k] - 1;

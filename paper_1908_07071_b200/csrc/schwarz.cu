@@ -343,7 +343,7 @@ __global__ void k_coarsest_factor(const double* __restrict__ A, double* __restri
 PatchGeom make_geom(const lorpc_prec* b) {
   PatchGeom G{};
   const lorpc_mesh* m = b->m;
-  G.d = m->d; G.kind = b->desc.patch_kind; G.L = b->lor->L;
+  G.d = m->d; G.kind = b->desc.patch_kind; G.L = b->lor->L; G.vz0 = b->pvz0;
   for (int k = 0; k < 3; ++k) G.n[k] = m->n[k];
   for (int l = 0; l < G.L; ++l) {
     G.ml[l] = b->lor->ml[l];
@@ -352,14 +352,68 @@ PatchGeom make_geom(const lorpc_prec* b) {
   return G;
 }
 
+// R_0 hierarchy on a vertex grid nv (reading c11): level 0 operator Ac0 (full
+// stencil, node-major; not owned), 2:1 Galerkin coarsening while every axis has
+// an even number (> 2) of intervals, dense Cholesky of the coarsest interior.
+int gmg_build(lorpc_prec* b, double* Ac0, const int* nv, int d, cudaStream_t s) {
+  b->nc = 0;
+  for (int i = 0; i < MAXC; ++i) { b->Ac[i] = b->dl1[i] = b->cr[i] = b->cz[i] = b->cs[i] = nullptr; }
+  int cur[3] = {nv[0], nv[1], d == 3 ? nv[2] : 1};
+  b->Ac[0] = Ac0;
+  int lvl = 0;
+  while (true) {
+    for (int k = 0; k < 3; ++k) b->cn[lvl][k] = cur[k];
+    b->cN[lvl] = (long long)cur[0] * cur[1] * cur[2];
+    LORPC_TRY(dalloc(&b->dl1[lvl], b->cN[lvl]));
+    LORPC_TRY(dalloc(&b->cr[lvl], b->cN[lvl]));
+    LORPC_TRY(dalloc(&b->cz[lvl], b->cN[lvl]));
+    LORPC_TRY(dalloc(&b->cs[lvl], b->cN[lvl]));
+    LORPC_CUDA(cudaMemsetAsync(b->cz[lvl], 0, sizeof(double) * b->cN[lvl], s));
+    LORPC_CUDA(cudaMemsetAsync(b->cs[lvl], 0, sizeof(double) * b->cN[lvl], s));
+    if (d == 2) k_l1diag<2><<<nb(b->cN[lvl], 256), 256, 0, s>>>(b->Ac[lvl], b->dl1[lvl], i3(cur));
+    else k_l1diag<3><<<nb(b->cN[lvl], 256), 256, 0, s>>>(b->Ac[lvl], b->dl1[lvl], i3(cur));
+    LORPC_LAUNCHED();
+    bool can = true;
+    for (int k = 0; k < d; ++k) if ((cur[k] - 1) % 2 != 0 || cur[k] - 1 <= 2) can = false;
+    if (!can || lvl + 1 >= MAXC) break;
+    int nxt[3] = {cur[0], cur[1], cur[2]};
+    for (int k = 0; k < d; ++k) nxt[k] = (cur[k] - 1) / 2 + 1;
+    long long Nn = (long long)nxt[0] * nxt[1] * nxt[2];
+    LORPC_TRY(dalloc(&b->Ac[lvl + 1], (size_t)ndp_of(d) * Nn));
+    int ne[3] = {nxt[0] - 1, nxt[1] - 1, nxt[2] - 1};
+    LORPC_TRY(galerkin(d, b->Ac[lvl], b->Ac[lvl + 1], gmg_transfer(), ne, cur, nxt, s));
+    for (int k = 0; k < 3; ++k) cur[k] = nxt[k];
+    ++lvl;
+  }
+  b->nc = lvl + 1;
+  int nint = 1;
+  for (int k = 0; k < d; ++k) nint *= b->cn[lvl][k] - 2;
+  if (nint > 64) return fail(LORPC_ERR_SIZE, "coarsest GMG level too large");
+  b->ncoarsest = nint;
+  LORPC_TRY(dalloc(&b->coarse_chol, (size_t)std::max(nint * nint, 1)));
+  if (nint > 0) {
+    if (d == 2) k_coarsest_factor<2><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
+    else k_coarsest_factor<3><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
+    LORPC_LAUNCHED();
+  }
+  return LORPC_OK;
+}
+
 int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   const lorpc_mesh* m = b->m;
   const lorpc_lor* lor = b->lor;
   const int d = m->d, L = lor->L, ND = d == 2 ? 9 : 27;
   b->L = L;
   PatchGeom G = make_geom(b);
-  if (b->desc.patch_kind == 0) b->J = (long long)(m->n[0] + 1) * (m->n[1] + 1) * (d == 3 ? m->n[2] + 1 : 1);
-  else b->J = m->nel;
+  if (b->desc.patch_kind == 0) {
+    const int nvz = d == 3 ? m->n[2] + 1 : 1;
+    if (b->pnvz <= 0) { b->pvz0 = 0; b->pnvz = nvz; }
+    if (b->pvz0 < 0 || b->pvz0 + b->pnvz > nvz) return fail(LORPC_ERR_ARG, "schwarz: patch plane range");
+    b->J = (long long)(m->n[0] + 1) * (m->n[1] + 1) * b->pnvz;
+  } else {
+    b->pvz0 = 0; b->pnvz = 0;
+    b->J = m->nel;
+  }
   // record offsets (host; patch sizes are index arithmetic)
   b->recoff_h.assign((size_t)b->J * L, 0);
   long long off = 0;
@@ -464,45 +518,8 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   b->nc = 0;
   for (int i = 0; i < MAXC; ++i) { b->Ac[i] = b->dl1[i] = b->cr[i] = b->cz[i] = b->cs[i] = nullptr; }
   if (b->desc.coarse == 0) {
-    int cur[3] = {m->n[0] + 1, m->n[1] + 1, d == 3 ? m->n[2] + 1 : 1};
-    b->Ac[0] = lor->A[L - 1];
-    int lvl = 0;
-    while (true) {
-      for (int k = 0; k < 3; ++k) b->cn[lvl][k] = cur[k];
-      b->cN[lvl] = (long long)cur[0] * cur[1] * cur[2];
-      LORPC_TRY(dalloc(&b->dl1[lvl], b->cN[lvl]));
-      LORPC_TRY(dalloc(&b->cr[lvl], b->cN[lvl]));
-      LORPC_TRY(dalloc(&b->cz[lvl], b->cN[lvl]));
-      LORPC_TRY(dalloc(&b->cs[lvl], b->cN[lvl]));
-      LORPC_CUDA(cudaMemsetAsync(b->cz[lvl], 0, sizeof(double) * b->cN[lvl], s));
-      LORPC_CUDA(cudaMemsetAsync(b->cs[lvl], 0, sizeof(double) * b->cN[lvl], s));
-      if (d == 2) k_l1diag<2><<<nb(b->cN[lvl], 256), 256, 0, s>>>(b->Ac[lvl], b->dl1[lvl], i3(cur));
-      else k_l1diag<3><<<nb(b->cN[lvl], 256), 256, 0, s>>>(b->Ac[lvl], b->dl1[lvl], i3(cur));
-      LORPC_LAUNCHED();
-      bool can = true;
-      for (int k = 0; k < d; ++k) if ((cur[k] - 1) % 2 != 0 || cur[k] - 1 <= 2) can = false;
-      if (!can || lvl + 1 >= MAXC) break;
-      int nxt[3] = {cur[0], cur[1], cur[2]};
-      for (int k = 0; k < d; ++k) nxt[k] = (cur[k] - 1) / 2 + 1;
-      long long Nn = (long long)nxt[0] * nxt[1] * nxt[2];
-      LORPC_TRY(dalloc(&b->Ac[lvl + 1], (size_t)ndp_of(d) * Nn));
-      int ne[3] = {nxt[0] - 1, nxt[1] - 1, nxt[2] - 1};
-      LORPC_TRY(galerkin(d, b->Ac[lvl], b->Ac[lvl + 1], gmg_transfer(), ne, cur, nxt, s));
-      for (int k = 0; k < 3; ++k) cur[k] = nxt[k];
-      ++lvl;
-    }
-    b->nc = lvl + 1;
-    // coarsest: dense Cholesky over its interior nodes
-    int nint = 1;
-    for (int k = 0; k < d; ++k) nint *= b->cn[lvl][k] - 2;
-    if (nint > 64) return fail(LORPC_ERR_SIZE, "coarsest GMG level too large");
-    b->ncoarsest = nint;
-    LORPC_TRY(dalloc(&b->coarse_chol, (size_t)std::max(nint * nint, 1)));
-    if (nint > 0) {
-      if (d == 2) k_coarsest_factor<2><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
-      else k_coarsest_factor<3><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
-      LORPC_LAUNCHED();
-    }
+    const int nv[3] = {m->n[0] + 1, m->n[1] + 1, d == 3 ? m->n[2] + 1 : 1};
+    LORPC_TRY(gmg_build(b, lor->A[L - 1], nv, d, s));
   }
   // dense coarse V-cycle operators: first level l >= 1 with <= 32 free nodes per patch
   // (the coarsest level if none); the V-cycle below it is one symmetric matrix

@@ -506,14 +506,10 @@ __global__ void __launch_bounds__(128) k_dense_coarse(VcParams P) {
 }
 
 // ------------------------------------------------------------------ apply driver
+// One GMG V(1,1) of R_0 (reading c11) on the hierarchy of gmg_build: input cr[0],
+// result in *out (cz[0] or cs[0]).
 template <int DIM>
-static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
-  const lorpc_mesh* m = b->m;
-  int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, DIM == 3 ? m->n[2] + 1 : 1);
-  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
-  int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
-  k_restrict_vertex<DIM><<<nb(b->cN[0], 128), 128, 0, s>>>(r, b->cr[0], nv, N, m->basis);
-  LORPC_LAUNCHED();
+static int gmg_vcycle_t(const lorpc_prec* b, const double** out, cudaStream_t s) {
   const int K = b->nc - 1;
   for (int l = 0; l < K; ++l) {
     int3 Nv = i3(b->cn[l]), Nc = i3(b->cn[l + 1]);
@@ -539,7 +535,32 @@ static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStr
     k_jacobi_post<DIM><<<nb(b->cN[l], 256), 256, 0, s>>>(b->Ac[l], b->cr[l], b->dl1[l], b->cz[l], b->cs[l], Nv);
     LORPC_LAUNCHED();
   }
-  const double* z0 = (K == 0) ? b->cz[0] : b->cs[0];
+  *out = (K == 0) ? b->cz[0] : b->cs[0];
+  return LORPC_OK;
+}
+// z += P_0 zc on the mesh's node grid (zc on its vertex grid; Dirichlet nodes set to 0)
+int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStream_t s) {
+  int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, m->d == 3 ? m->n[2] + 1 : 1);
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]), n = make_int3(m->n[0], m->n[1], m->n[2]);
+  if (m->d == 2) k_prolong_vertex_add<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
+  else k_prolong_vertex_add<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+int gmg_vcycle(const lorpc_prec* b, const double** out, cudaStream_t s) {
+  return b->m->d == 2 ? gmg_vcycle_t<2>(b, out, s) : gmg_vcycle_t<3>(b, out, s);
+}
+
+template <int DIM>
+static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  const lorpc_mesh* m = b->m;
+  int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, DIM == 3 ? m->n[2] + 1 : 1);
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
+  int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
+  k_restrict_vertex<DIM><<<nb(b->cN[0], 128), 128, 0, s>>>(r, b->cr[0], nv, N, m->basis);
+  LORPC_LAUNCHED();
+  const double* z0 = nullptr;
+  LORPC_TRY(gmg_vcycle_t<DIM>(b, &z0, s));
   k_prolong_vertex_add<DIM><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z0, z, nv, N, n, m->basis);
   LORPC_LAUNCHED();
   return LORPC_OK;
@@ -599,6 +620,14 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
 int dense_coarse_setup(lorpc_prec* b, cudaStream_t s) {
   VcParams P = make_params(b, nullptr, nullptr);
   return b->m->d == 2 ? launch_vc<2, true>(P, b->J, s) : launch_vc<3, true>(P, b->J, s);
+}
+
+// z = sum_j I_j B_j I_j^T r over the patches (no coarse term, z not zeroed at Dirichlet nodes)
+int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * b->m->ndof_cg, s));
+  if (b->tmode) return vcycle_t_apply(b, r, z, s);
+  VcParams P = make_params(b, r, z);
+  return b->m->d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
 }
 
 int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {

@@ -34,7 +34,7 @@ static std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
   const lorpc_mesh* m = b->m;
   const int d = m->d, star = b->desc.patch_kind == 1;
   const int gx = m->n[0] + (star ? 0 : 1), gy = m->n[1] + (star ? 0 : 1);
-  const int gz = d == 3 ? m->n[2] + (star ? 0 : 1) : 1;
+  const int gz = d == 3 ? (star ? m->n[2] : b->pnvz) : 1;
   const long long nw = (b->J + 31) / 32;
   std::vector<int> ord;
   ord.reserve((size_t)(nw * 32));

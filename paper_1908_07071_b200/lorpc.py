@@ -45,7 +45,16 @@ SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc
            "lorpc_schwarz_setup", "lorpc_prec_destroy", "lorpc_precond_apply",
            "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_prec_bytes", "lorpc_prec_profile",
            "lorpc_prec_profile_read", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
-           "lorpc_launch_count", "lorpc_last_error"]
+           "lorpc_launch_count", "lorpc_last_error",
+           "lorpc_dist_plan_get", "lorpc_dist_nccl_id", "lorpc_dist_create", "lorpc_dist_destroy",
+           "lorpc_dist_info", "lorpc_dist_operator_apply", "lorpc_dist_precond_apply", "lorpc_dist_pcg_solve"]
+
+
+class DistPlan(ctypes.Structure):
+    _fields_ = [("z0", _int), ("z1", _int), ("za", _int), ("zb", _int), ("own_plane0", _int),
+                ("own_planes", _int), ("gown_plane0", _int), ("vown0", _int), ("nvown", _int),
+                ("to", _int * 4), ("from_", _int * 4), ("send0", _int * 4), ("recv0", _int * 4),
+                ("nplanes", _int * 4)]
 
 
 def lib():
@@ -75,6 +84,16 @@ def lib():
         L.lorpc_pcg_solve_host.argtypes = [_vp, _vp, _vp, _vp, _d, _int, ctypes.POINTER(PcgReport), _vp]
         L.lorpc_launch_count.restype = _ll
         L.lorpc_launch_count.argtypes = [_int]
+        L.lorpc_dist_plan_get.argtypes = [_int, _int, _int, _int, ctypes.POINTER(DistPlan)]
+        L.lorpc_dist_nccl_id.argtypes = [_vp]
+        L.lorpc_dist_create.argtypes = [ctypes.POINTER(MeshDesc), _vp, ctypes.POINTER(SchwarzDesc), _int, _int, _vp,
+                                        _vp, ctypes.POINTER(_vp)]
+        L.lorpc_dist_destroy.argtypes = [_vp]
+        L.lorpc_dist_info.argtypes = [_vp, _int, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
+        L.lorpc_dist_operator_apply.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        L.lorpc_dist_precond_apply.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+        L.lorpc_dist_pcg_solve.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _d, _int,
+                                           ctypes.POINTER(PcgReport)]
         _lib = L
     return _lib
 
@@ -228,3 +247,68 @@ def pcg_solve_host(mesh, prec, b_host, x_host, rtol, maxit=2000, stream=None):
     _check(lib().lorpc_pcg_solve_host(mesh.h, prec.h, b_host.ctypes.data, x_host.ctypes.data, float(rtol),
                                       int(maxit), ctypes.byref(rep), _stream(stream)))
     return _report(rep, maxit, keep)
+
+
+# ---------------------------------------------------------------- multi-GPU slabs
+def dist_plan(n_z, p, nranks, rank):
+    """Slab plan of one rank (host-only C call): ownership and the four exchange phases."""
+    P = DistPlan()
+    _check(lib().lorpc_dist_plan_get(int(n_z), int(p), int(nranks), int(rank), ctypes.byref(P)))
+    return {"z0": P.z0, "z1": P.z1, "za": P.za, "zb": P.zb, "own_plane0": P.own_plane0,
+            "own_planes": P.own_planes, "gown_plane0": P.gown_plane0, "vown0": P.vown0, "nvown": P.nvown,
+            "to": list(P.to), "from": list(P.from_), "send0": list(P.send0), "recv0": list(P.recv0),
+            "nplanes": list(P.nplanes)}
+
+
+def dist_nccl_id():
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().lorpc_dist_nccl_id(ctypes.cast(buf, _vp)))
+    return bytes(buf)
+
+
+class Dist:
+    """lorpc_dist: the C5-style slab decomposition of the 3D CG path.
+
+    nccl_id=None: all `nranks` ranks emulated in this process on the current device
+    (exchanges by device copies); otherwise this process is rank `rank` of an NCCL
+    communicator."""
+
+    def __init__(self, n, p, vertices, nranks, rank=0, nccl_id=None, patch_kind="vertex", ordering="mdf",
+                 stream=None):
+        self.desc = MeshDesc(3, (_int * 3)(*n), p, 0, 0.0)
+        self.sdesc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], 0)
+        V = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._id = (ctypes.c_ubyte * 128)(*nccl_id) if nccl_id is not None else None
+        h = _vp()
+        _check(lib().lorpc_dist_create(ctypes.byref(self.desc), V.ctypes.data, ctypes.byref(self.sdesc),
+                                       int(nranks), int(rank), ctypes.cast(self._id, _vp) if self._id else None,
+                                       _stream(stream), ctypes.byref(h)))
+        self.h = h
+        self.nranks = nranks
+        self.nlocal = nranks if nccl_id is None else 1
+        self.owned = []
+        for i in range(self.nlocal):
+            off, cnt, J = _ll(), _ll(), _ll()
+            _check(lib().lorpc_dist_info(self.h, i, ctypes.byref(off), ctypes.byref(cnt), ctypes.byref(J)))
+            self.owned.append((off.value, cnt.value, J.value))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.lorpc_dist_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def _ptrs(ts):
+        return (_vp * len(ts))(*[_dptr(t) for t in ts])
+
+    def apply(self, xs, ys):
+        _check(lib().lorpc_dist_operator_apply(self.h, self._ptrs(xs), self._ptrs(ys)))
+
+    def precond(self, rs, zs):
+        _check(lib().lorpc_dist_precond_apply(self.h, self._ptrs(rs), self._ptrs(zs)))
+
+    def pcg_solve(self, bs, xs, rtol, maxit=2000):
+        rep, keep = _mkrep(maxit)
+        _check(lib().lorpc_dist_pcg_solve(self.h, self._ptrs(bs), self._ptrs(xs), float(rtol), int(maxit),
+                                          ctypes.byref(rep)))
+        return _report(rep, maxit, keep)
