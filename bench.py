@@ -258,7 +258,8 @@ def run_lorpc(args):
                        "l2": "inputs larger than L2 (working set >> 126 MB)" if mesh.n_dof > 4_000_000
                        else "L2-resident working set (no flush; latency case)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_vcycle (patch V-cycle)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "patch V-cycle apply (k_vt_smooth pre + k_vt_mid + k_vt_smooth post)",
                          "algorithmic_bytes_per_launch": vc_bytes, "launch_ms": per_launch_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * mesh.n_dof,
