@@ -282,3 +282,42 @@ def test_dg_precond_and_pcg_parity(L, name):
     k = min(len(rep["res"]), len(ro["res"])) // 3
     assert np.allclose(rep["res"][:k], ro["res"][:k], rtol=1e-3)
     assert rel(x.cpu().numpy(), xo) <= 1e-8
+
+
+def test_full_size_c5_preconditioner_and_pcg(L):
+    """C5 at full size in the bench's launch configuration (thread-mode V-cycle):
+    properties that hold at any size — B symmetric positive definite (reading c5
+    makes the V-cycle symmetric, eq:as sums SPD terms) — and the h-independence of
+    the PCG iteration count (Cor. cor:as): the 128^3 solve needs within +-3
+    iterations of the oracle's solve of the same recipe on 16^3."""
+    cfg = get_config("C5")
+    mesh = gpu_problem(L, cfg)
+    prec = L.Prec(L.Lor(mesh), patch_kind=cfg.patch_kind)
+    n = mesh.n_dof
+    rng = np.random.default_rng(5)
+    r1, r2 = rng.standard_normal(n), rng.standard_normal(n)
+    # zero the Dirichlet rows (grid boundary)
+    N = cfg.n[0] * cfg.p + 1
+    g = np.arange(n)
+    ix, iy, iz = g % N, (g // N) % N, g // (N * N)
+    bd = (ix == 0) | (ix == N - 1) | (iy == 0) | (iy == N - 1) | (iz == 0) | (iz == N - 1)
+    r1[bd] = 0.0
+    r2[bd] = 0.0
+    z1 = torch.empty(n, dtype=torch.float64, device="cuda")
+    z2 = torch.empty_like(z1)
+    prec.apply(dev(r1), z1)
+    prec.apply(dev(r2), z2)
+    z1h, z2h = z1.cpu().numpy(), z2.cpu().numpy()
+    a, b = float(z1h @ r2), float(r1 @ z2h)
+    assert abs(a - b) <= 1e-12 * (abs(a) + abs(b)) + 1e-14 * np.linalg.norm(z1h) * np.linalg.norm(r2)
+    assert float(z1h @ r1) > 0 and float(z2h @ r2) > 0
+    assert np.all(z1h[bd] == 0.0)
+    b_rhs = random_free_rhs(cfg)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    rep = L.pcg_solve(mesh, prec, dev(b_rhs), x, cfg.tol)
+    assert rep["converged"] and rep["rel_res"] <= cfg.tol
+    small = small_config("C5", (16, 16, 16))
+    P = O.Problem.from_config(small)
+    P.schwarz_setup("vertex", "mdf", "gmg")
+    _, ro = P.pcg(random_free_rhs(small), small.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 3, (rep["iters"], ro["iters"])
