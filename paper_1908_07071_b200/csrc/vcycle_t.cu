@@ -74,6 +74,13 @@ __host__ __device__ __forceinline__ TRecLayout trec_layout(int S, int Kp) {
   return T;
 }
 
+// Pair rows per step are padded up to a class {0, 1, 2, 4, 7, 10, 13}: the sweeps
+// run a compile-time-sized body per class (no per-step dispatch inside a run of
+// equal classes; the MDF columns of a patch plateau at 6-7 pairs).
+__host__ __device__ __forceinline__ int tclass(int mp) {
+  return mp <= 2 ? mp : mp <= 4 ? 4 : mp <= 7 ? 7 : mp <= 10 ? 10 : 13;
+}
+
 struct TRecParams {
   const char* rec;
   const long long* recoff;
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, in
   int Kp = 0;
   for (int t = 0; t < S; ++t) {
     const unsigned cb = t < n ? brp[t + 1] - brp[t] : 0u;
-    Kp += (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
+    Kp += tclass((int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2));
   }
   const TRecLayout T = trec_layout(S, Kp);
   if (!fill) {
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, in
       b0 = brp[t]; cb = brp[t + 1] - b0;
       dv = 1.0 / Dn[node];
     }
-    const int mp = (int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2);
+    const int mp = tclass((int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2));
     H[t * 32 + lane] = (uint32_t)node | (cb << 8) | ((uint32_t)mp << 16);
     Dd[t * 32 + lane] = dv;
     for (int k = 0; k < 2 * mp; ++k) {
@@ -278,180 +285,178 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 // consecutive nodes of one patch.  X points at the lane's column (word q).
 #define VO(i, q) ((i) * 33 + (q))
 
-// One sweep step's column data, register-resident (NP = max pairs per column)
-template <int NP>
+// One step's column data in registers: MP pair rows (compile-time class size)
+template <int MP>
 struct TStage {
-  double2 l[NP];
-  uint32_t c[NP];
+  double2 l[MP > 0 ? MP : 1];
+  uint32_t c[MP > 0 ? MP : 1];
 };
-// Loads of one step: mp pair rows (warp-uniform) from pair row kp.  Lanes whose
-// column is shorter skip the value loads of their padding pairs (no memory
-// traffic); stale register values there meet the dummy node (see tfwd / tbwd), so
-// the stage starts finite (zeroed).  The node indices are always loaded (padding
-// holds the dummy).  Entered by a jump into a fall-through sequence.
-#define LORPC_TL_PAIR(P_)                                            \
-  if ((P_) < NP) {                                                   \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                         \
-    if (2 * pp < cnt) s.l[pp] = __ldcs(Lq + pp * 32);                \
-    s.c[pp] = __ldcs(Cq + pp * 32);                                  \
-  }
-template <int NP>
-__device__ __forceinline__ void tload(TStage<NP>& s, const double2* __restrict__ Lp, const uint16_t* __restrict__ Cp,
-                                      int kp, int mp, int cnt) {
-  const double2* Lq = Lp + (long long)kp * 32;
-  const uint16_t* Cq = Cp + (long long)kp * 32;
-  switch (mp) {
-    case 13: LORPC_TL_PAIR(12); [[fallthrough]];
-    case 12: LORPC_TL_PAIR(11); [[fallthrough]];
-    case 11: LORPC_TL_PAIR(10); [[fallthrough]];
-    case 10: LORPC_TL_PAIR(9); [[fallthrough]];
-    case 9: LORPC_TL_PAIR(8); [[fallthrough]];
-    case 8: LORPC_TL_PAIR(7); [[fallthrough]];
-    case 7: LORPC_TL_PAIR(6); [[fallthrough]];
-    case 6: LORPC_TL_PAIR(5); [[fallthrough]];
-    case 5: LORPC_TL_PAIR(4); [[fallthrough]];
-    case 4: LORPC_TL_PAIR(3); [[fallthrough]];
-    case 3: LORPC_TL_PAIR(2); [[fallthrough]];
-    case 2: LORPC_TL_PAIR(1); [[fallthrough]];
-    case 1: LORPC_TL_PAIR(0); [[fallthrough]];
-    default: break;
+template <int MP>
+__device__ __forceinline__ void tload(TStage<MP>& g, const double2* __restrict__ Lp, const uint16_t* __restrict__ Cp,
+                                      int kp) {
+#pragma unroll
+  for (int p = 0; p < MP; ++p) {
+    g.l[p] = __ldcs(Lp + (long long)(kp + p) * 32);
+    g.c[p] = __ldcs(Cp + (long long)(kp + p) * 32);
   }
 }
-#undef LORPC_TL_PAIR
-
-// forward (push) step: yk = X[k]; X[i] -= L_ik yk for the column; X[k] = yk / D_k.
-// All neighbour values are loaded before any is stored (the column's nodes are
-// distinct, padding aside), so the loads issue back to back.
-#define LORPC_FL(P_)                                                      \
-  if ((P_) < NP) {                                                        \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
-    v0[pp] = X[33 * (s.c[pp] & 0xff)];                                    \
-    v1[pp] = X[33 * (s.c[pp] >> 8)];                                      \
-  }
-#define LORPC_FS(P_)                                                      \
-  if ((P_) < NP) {                                                        \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
-    X[33 * (s.c[pp] & 0xff)] = v0[pp] - s.l[pp].x * yk;                   \
-    X[33 * (s.c[pp] >> 8)] = v1[pp] - s.l[pp].y * yk;                     \
-  }
-#define LORPC_CASES(M_)                                                   \
-  switch (mp) {                                                           \
-    case 13: M_(12); [[fallthrough]];                                     \
-    case 12: M_(11); [[fallthrough]];                                     \
-    case 11: M_(10); [[fallthrough]];                                     \
-    case 10: M_(9); [[fallthrough]];                                      \
-    case 9: M_(8); [[fallthrough]];                                       \
-    case 8: M_(7); [[fallthrough]];                                       \
-    case 7: M_(6); [[fallthrough]];                                       \
-    case 6: M_(5); [[fallthrough]];                                       \
-    case 5: M_(4); [[fallthrough]];                                       \
-    case 4: M_(3); [[fallthrough]];                                       \
-    case 3: M_(2); [[fallthrough]];                                       \
-    case 2: M_(1); [[fallthrough]];                                       \
-    case 1: M_(0); [[fallthrough]];                                       \
-    default: break;                                                       \
-  }
-template <int NP>
-__device__ __forceinline__ void tfwd_step(const TStage<NP>& s, int mp, uint32_t h, double dinv, double* X) {
+// forward (push) step: yk = X[k]; X[i] -= L_ik yk over the column; X[k] = yk / D_k.
+// All neighbour values are loaded before any is stored (the nodes of a column are
+// distinct; padding entries carry L = 0 and the dummy node).
+template <int MP>
+__device__ __forceinline__ void tfwd_step(const TStage<MP>& g, uint32_t h, double dinv, double* X) {
   const int k = h & 0xff;
   const double yk = X[33 * k];
-  double v0[NP], v1[NP];
-  LORPC_CASES(LORPC_FL)
-  LORPC_CASES(LORPC_FS)
+  double v0[MP > 0 ? MP : 1], v1[MP > 0 ? MP : 1];
+#pragma unroll
+  for (int p = 0; p < MP; ++p) { v0[p] = X[33 * (g.c[p] & 0xff)]; v1[p] = X[33 * (g.c[p] >> 8)]; }
+#pragma unroll
+  for (int p = 0; p < MP; ++p) {
+    X[33 * (g.c[p] & 0xff)] = v0[p] - g.l[p].x * yk;
+    X[33 * (g.c[p] >> 8)] = v1[p] - g.l[p].y * yk;
+  }
   X[33 * k] = yk * dinv;
 }
 // backward (pull) step: X[k] -= sum_i L_ik X[i]; four partial sums
-#define LORPC_BD(P_)                                                      \
-  if ((P_) < NP) {                                                        \
-    constexpr int pp = (P_) < NP ? (P_) : 0;                              \
-    a[2 * (pp & 1)] -= s.l[pp].x * X[33 * (s.c[pp] & 0xff)];              \
-    a[2 * (pp & 1) + 1] -= s.l[pp].y * X[33 * (s.c[pp] >> 8)];            \
-  }
-template <int NP>
-__device__ __forceinline__ void tbwd_step(const TStage<NP>& s, int mp, uint32_t h, double* X) {
+template <int MP>
+__device__ __forceinline__ void tbwd_step(const TStage<MP>& g, uint32_t h, double* X) {
   const int k = h & 0xff;
   double a[4] = {X[33 * k], 0.0, 0.0, 0.0};
-  LORPC_CASES(LORPC_BD)
+#pragma unroll
+  for (int p = 0; p < MP; ++p) {
+    a[2 * (p & 1)] -= g.l[p].x * X[33 * (g.c[p] & 0xff)];
+    a[2 * (p & 1) + 1] -= g.l[p].y * X[33 * (g.c[p] >> 8)];
+  }
   X[33 * k] = (a[0] + a[1]) + (a[2] + a[3]);
 }
-#undef LORPC_FL
-#undef LORPC_FS
-#undef LORPC_BD
+
+// Sweep cursor over a T-record block (lane-adjusted pointers)
+struct TSw {
+  const uint32_t* H;    // header of step index 0 of the sweep order is H0; step s at H0 + s * dir
+  const double* Dd;     // Dinv[t][lane] base
+  const double2* Lp;    // pair rows [Kp][32] base
+  const uint16_t* Cp;
+  int S, Kp, s;         // steps, pair rows, current step (sweep order)
+  int kp;               // forward: first pair row of step s; backward: one past its last
+  uint32_t hc, hn;      // headers of steps s and s + 1 (0 past the end)
+  int pf, TPFD, lane;   // L2 prefetch cursor / distance
+};
+template <bool BWD>
+__device__ __forceinline__ int tstep_t(const TSw& W, int s) { return BWD ? W.S - 1 - s : s; }
+template <bool BWD>
+__device__ __forceinline__ void tprefetch(TSw& W, int kp) {
+  if (W.lane != 0) return;
+  if (!BWD) {
+    while (W.pf < W.Kp && W.pf < kp + W.TPFD) {
+      const int nr = min(8, W.Kp - W.pf);
+      l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
+      l2_prefetch(W.Cp - W.lane + W.pf * 32, 64u * nr);
+      W.pf += nr;
+    }
+  } else {
+    while (W.pf > 0 && W.pf > kp - W.TPFD) {
+      const int nr = min(8, W.pf);
+      W.pf -= nr;
+      l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
+      l2_prefetch(W.Cp - W.lane + W.pf * 32, 64u * nr);
+    }
+  }
+}
+__device__ __forceinline__ int mpof(uint32_t h) { return (int)((h >> 16) & 0xffu); }
+
+// A run of consecutive steps of class MP, one step of software pipelining (the
+// next step's column is loaded while the current one is applied; the register
+// stages swap roles by the two-step unroll).  Returns at a class change or the end.
+template <int MP, bool BWD>
+__device__ __forceinline__ void trun(TSw& W, double* X) {
+  const int dir = BWD ? -32 : 32;
+  if constexpr (MP > 7) {
+    // wide columns (rare): no pipelining, one register stage
+    for (;;) {
+      TStage<MP> A;
+      const int kpA = BWD ? W.kp - MP : W.kp;
+      tload<MP>(A, W.Lp, W.Cp, kpA);
+      const double dA = BWD ? 1.0 : __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s));
+      const uint32_t h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
+      tprefetch<BWD>(W, kpA);
+      if (BWD) tbwd_step<MP>(A, W.hc, X); else tfwd_step<MP>(A, W.hc, dA, X);
+      W.s += 1; W.hc = W.hn; W.hn = h2;
+      W.kp = BWD ? kpA : kpA + MP;
+      if (!(W.s < W.S && mpof(W.hc) == MP)) return;
+    }
+  }
+  TStage<MP> A, B;
+  int kpA = BWD ? W.kp - MP : W.kp;
+  tload<MP>(A, W.Lp, W.Cp, kpA);
+  double dA = BWD ? 1.0 : __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s));
+  for (;;) {
+    // step s from A; B <- step s + 1 if it is of the same class
+    const bool c1 = W.s + 1 < W.S && mpof(W.hn) == MP;
+    const int kpB = BWD ? kpA - MP : kpA + MP;
+    double dB = 1.0;
+    if (c1) {
+      tload<MP>(B, W.Lp, W.Cp, kpB);
+      if (!BWD) dB = __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s + 1));
+    }
+    uint32_t h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
+    tprefetch<BWD>(W, kpA);
+    if (BWD) tbwd_step<MP>(A, W.hc, X); else tfwd_step<MP>(A, W.hc, dA, X);
+    W.s += 1; W.hc = W.hn; W.hn = h2;
+    W.kp = BWD ? kpA : kpA + MP;
+    if (!c1) return;
+    // step s + 1 from B; A <- step s + 2 if it is of the same class
+    const bool c2 = W.s + 1 < W.S && mpof(W.hn) == MP;
+    kpA = BWD ? kpB - MP : kpB + MP;
+    if (c2) {
+      tload<MP>(A, W.Lp, W.Cp, kpA);
+      if (!BWD) dA = __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s + 1));
+    }
+    h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
+    if (BWD) tbwd_step<MP>(B, W.hc, X); else tfwd_step<MP>(B, W.hc, dB, X);
+    W.s += 1; W.hc = W.hn; W.hn = h2;
+    W.kp = BWD ? kpB : kpB + MP;
+    if (!c2) return;
+  }
+}
 
 // One triangular sweep of the lane's own patch over the T-record block: forward
-// (push, steps ascending, diagonal fused) or backward (pull, steps descending).
-// Software-pipelined one step deep (unrolled by two so that the register stages
-// swap roles without moves): the next step's column is loaded while the current
-// one is applied, and the record streams through L2 prefetches TPFD pair rows
-// ahead.  X = the lane's column of the warp's shared vectors; X[33 * dummy] must be
-// zero on entry to the backward sweep (padding entries read it).
+// (push, steps ascending, diagonal fused) or backward (pull, steps descending),
+// dispatched once per run of equal step classes.  The record streams through L2
+// prefetches TPFD pair rows ahead.  X = the lane's column of the warp's shared
+// vectors; X[33 * dummy] must be zero on entry to the backward sweep.
 template <int NP, bool BWD>
 __device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
   const int4 hd = __ldg((const int4*)blk);
-  const int S = hd.x, Kp = hd.y;
-  if (S == 0) return;
-  const TRecLayout T = trec_layout(S, Kp);
-  const int dir = BWD ? -32 : 32;
-  const uint32_t* H = (const uint32_t*)(blk + T.hdr) + lane + (BWD ? (S - 1) * 32 : 0);
-  const double* Dd = (const double*)(blk + T.D) + lane;
-  const double2* Lp = (const double2*)(blk + T.Lc) + lane;
-  const uint16_t* Cp = (const uint16_t*)(blk + T.Ic) + lane;
-  // L2 prefetch cursor (pair rows; forward ascending, backward descending)
-  int pf = 0;
-  auto prefetch = [&](int kp) {
-    if (lane != 0) return;
-    if (!BWD) {
-      while (pf < Kp && pf < kp + TPFD) {
-        const int nr = min(8, Kp - pf);
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-        l2_prefetch(Cp - lane + pf * 32, 64u * nr);
-        pf += nr;
-      }
-    } else {
-      while (pf > 0 && pf > kp - TPFD) {
-        const int nr = min(8, pf);
-        pf -= nr;
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-        l2_prefetch(Cp - lane + pf * 32, 64u * nr);
-      }
-    }
-  };
+  TSw W;
+  W.S = hd.x; W.Kp = hd.y;
+  if (W.S == 0) return;
+  const TRecLayout T = trec_layout(W.S, W.Kp);
+  W.H = (const uint32_t*)(blk + T.hdr) + lane + (BWD ? (W.S - 1) * 32 : 0);
+  W.Dd = (const double*)(blk + T.D) + lane;
+  W.Lp = (const double2*)(blk + T.Lc) + lane;
+  W.Cp = (const uint16_t*)(blk + T.Ic) + lane;
+  W.TPFD = TPFD; W.lane = lane;
+  W.pf = BWD ? W.Kp : 0;
   if (lane == 0) {
-    l2_prefetch((const uint32_t*)(blk + T.hdr), 128u * S);
-    if (!BWD) l2_prefetch((const double*)(blk + T.D), 256u * S);
-    pf = BWD ? Kp : 0;
+    l2_prefetch((const uint32_t*)(blk + T.hdr), 128u * W.S);
+    if (!BWD) l2_prefetch((const double*)(blk + T.D), 256u * W.S);
   }
-  auto mpof = [](uint32_t h) { return (int)((h >> 16) & 0xffu); };
-  auto cntof = [](uint32_t h) { return (int)((h >> 8) & 0xffu); };
-  TStage<NP> A, B;
-#pragma unroll
-  for (int p = 0; p < NP; ++p) { A.l[p] = B.l[p] = make_double2(0.0, 0.0); A.c[p] = B.c[p] = 0u; }
-  const int t0 = BWD ? S - 1 : 0;
-  uint32_t h0 = __ldg(H), h1 = S > 1 ? __ldg(H + dir) : 0u;
-  double d0 = BWD ? 1.0 : __ldg(Dd + 32 * t0), d1 = !BWD && S > 1 ? __ldg(Dd + 32) : 1.0;
-  int m0 = mpof(h0);
-  int kp = BWD ? Kp - m0 : 0;  // first pair row of the current step
-  prefetch(kp);
-  tload<NP>(A, Lp, Cp, kp, m0, cntof(h0));
-  for (int s = 0; s < S; s += 2) {
-    // step s: A current, B <- step s + 1
-    const uint32_t h2 = s + 2 < S ? __ldg(H + 2 * dir) : 0u;
-    const double d2 = !BWD && s + 2 < S ? __ldg(Dd + 32 * (s + 2)) : 1.0;
-    const int m1 = mpof(h1);
-    const int kp1 = BWD ? kp - m1 : kp + m0;
-    prefetch(kp);
-    if (s + 1 < S) tload<NP>(B, Lp, Cp, kp1, m1, cntof(h1));
-    if (BWD) tbwd_step<NP>(A, m0, h0, X); else tfwd_step<NP>(A, m0, h0, d0, X);
-    if (s + 1 >= S) break;
-    // step s + 1: B current, A <- step s + 2
-    const uint32_t h3 = s + 3 < S ? __ldg(H + 3 * dir) : 0u;
-    const double d3 = !BWD && s + 3 < S ? __ldg(Dd + 32 * (s + 3)) : 1.0;
-    const int m2 = mpof(h2);
-    const int kp2 = BWD ? kp1 - m2 : kp1 + m1;
-    if (s + 2 < S) tload<NP>(A, Lp, Cp, kp2, m2, cntof(h2));
-    if (BWD) tbwd_step<NP>(B, m1, h1, X); else tfwd_step<NP>(B, m1, h1, d1, X);
-    H += 2 * dir;
-    h0 = h2; h1 = h3; d0 = d2; d1 = d3; m0 = m2; kp = kp2;
+  W.s = 0;
+  W.kp = BWD ? W.Kp : 0;
+  const int dir = BWD ? -32 : 32;
+  W.hc = __ldg(W.H);
+  W.hn = W.S > 1 ? __ldg(W.H + dir) : 0u;
+  tprefetch<BWD>(W, W.kp);
+  while (W.s < W.S) {
+    switch (mpof(W.hc)) {
+      case 0: trun<0, BWD>(W, X); break;
+      case 1: trun<1, BWD>(W, X); break;
+      case 2: trun<2, BWD>(W, X); break;
+      case 4: trun<4, BWD>(W, X); break;
+      case 7: if (NP >= 7) trun<(NP >= 7 ? 7 : 1), BWD>(W, X); break;
+      case 10: if (NP >= 10) trun<(NP >= 10 ? 10 : 1), BWD>(W, X); break;
+      default: if (NP >= 13) trun<(NP >= 13 ? 13 : 1), BWD>(W, X); break;
+    }
   }
 }
 
