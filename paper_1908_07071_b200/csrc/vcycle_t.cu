@@ -646,6 +646,179 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
   }
 }
 
+// 3D line variant (patch boxes of at most 5 nodes per axis, p <= 3): the lane
+// walks its patch by x-lines.  For each line the 3 x 3 neighbouring lines of the
+// patch vector are read once into registers (zero outside the box) and the five
+// residuals use them with compile-time indices, so a node costs its LOR row (7
+// 256-bit loads) and 27 FMAs instead of 27 predicated vector loads; restriction and
+// prolongation are separable per line (3 FMAs per node, 27 per line).
+constexpr int TLX = 5;  // largest box extent of the line variant
+template <bool RESTRICT>
+__device__ __forceinline__ void tline_residual(const TcParams& P, const TPatch& c, const double* __restrict__ V,
+                                               int iy, int iz, double* res) {
+  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
+  const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+  const long long g0 = c.lo[0] + Nx * ((c.lo[1] + iy) + Ny * (long long)(c.lo[2] + iz));
+  // neighbouring lines (dy, dz) of V; column xx = x + 1, x in [-1, ex]
+  const double* L[3][3];
+  bool ok[3][3];
+#pragma unroll
+  for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      const int yy = iy + dy - 1, zz = iz + dz - 1;
+      ok[dz][dy] = yy >= 0 && yy < ey && zz >= 0 && zz < ez;
+      L[dz][dy] = V + (long long)((ok[dz][dy] ? zz * ey + yy : 0) * ex) * 32;
+    }
+  // columns are loaded one node ahead (column x + 2 at node x), so only a
+  // 3-column window of the 3 x 3 lines is live
+  double W[3][3][TLX + 2];
+#pragma unroll
+  for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      W[dz][dy][0] = 0.0;
+      W[dz][dy][1] = ok[dz][dy] ? L[dz][dy][0] : 0.0;
+    }
+#pragma unroll
+  for (int x = 0; x < TLX; ++x) {
+    if (x >= ex) break;
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? L[dz][dy][(x + 1) * 32] : 0.0;
+    const long long gi = g0 + x;
+    const double* Ar = P.A0 + (size_t)gi * 28;
+    double a0 = __ldg(P.r + gi), a1 = 0.0;
+#pragma unroll
+    for (int d4 = 0; d4 < 7; ++d4) {
+      double av[4];
+      ld256(Ar + 4 * d4, av[0], av[1], av[2], av[3]);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int d = 4 * d4 + h;
+        if (d >= 27) break;
+        // x + 1 + dx is within [0, ex + 1]; columns past ex are zero
+        const double v = (x + 2 + dir_dx(d) <= TLX + 1) ? W[dir_dz(d) + 1][dir_dy(d) + 1][x + 1 + dir_dx(d)] : 0.0;
+        if (h & 1) a1 -= av[h] * v; else a0 -= av[h] * v;
+      }
+    }
+    res[x] = a0 + a1;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
+  constexpr int NC = 27, NPK = TCoarse<3>::NPK;
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (slot >= P.nslots) return;
+  const long long j = P.pord[slot];
+  if (j < 0) return;
+  const long long w = slot >> 5;
+  const int lane = threadIdx.x & 31;
+  const TPatch c = tpatch<3>(P.G, j);
+  const TWalk wk = twalk<3>(P.G, c, j);
+  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
+  const long long col = w * (long long)P.n0max * 32 + lane;
+  const double* Xp = P.xpark + col;
+  double* Yp = P.ypark + col;
+  double* Sp = P.spark + col;
+  const double* Wx = P.W + P.woff[c.ec[0]];
+  const double* Wy = P.W + P.woff[c.ec[1]];
+  const double* Wz = P.W + P.woff[c.ec[2]];
+  auto wt = [](const double* T, int k, int ce, int e, int i) { return k < ce ? __ldg(T + k * e + i) : 0.0; };
+  // s = r - A x and r_1 = P^T s
+  double r1[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) r1[k] = 0.0;
+  for (int kz = 0; kz < ez; ++kz) {
+    const int iz = wk.fz ? ez - 1 - kz : kz;
+    for (int ky = 0; ky < ey; ++ky) {
+      const int iy = wk.fy ? ey - 1 - ky : ky;
+      double res[TLX];
+      tline_residual<true>(P, c, Xp, iy, iz, res);
+      double t[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int x = 0; x < TLX; ++x) {
+        if (x >= ex) break;
+#pragma unroll
+        for (int cx = 0; cx < 3; ++cx) t[cx] += wt(Wx, cx, c.cext[0], ex, x) * res[x];
+      }
+      double wy[3], wz[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
+#pragma unroll
+      for (int cz = 0; cz < 3; ++cz)
+#pragma unroll
+        for (int cy = 0; cy < 3; ++cy) {
+          const double f = wy[cy] * wz[cz];
+#pragma unroll
+          for (int cx = 0; cx < 3; ++cx) r1[cx + 3 * (cy + 3 * cz)] += f * t[cx];
+        }
+    }
+  }
+  // z_1 = C r_1 (packed symmetric, fixed coarse box, interleaved by lane)
+  double z1[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) z1[k] = 0.0;
+  {
+    const double* C = P.Cp + w * 32ll * NPK + lane;
+    int idx = 0;
+#pragma unroll
+    for (int a = 0; a < NC; ++a) {
+#pragma unroll
+      for (int b = a; b < NC; ++b) {
+        const double cv = __ldcs(C + 32 * idx);
+        z1[a] += cv * r1[b];
+        if (b != a) z1[b] += cv * r1[a];
+        ++idx;
+      }
+    }
+  }
+  // y = x + P z_1, by lines
+  for (int kz = 0; kz < ez; ++kz) {
+    const int iz = wk.fz ? ez - 1 - kz : kz;
+    for (int ky = 0; ky < ey; ++ky) {
+      const int iy = wk.fy ? ey - 1 - ky : ky;
+      double wy[3], wz[3], u[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
+#pragma unroll
+      for (int cz = 0; cz < 3; ++cz)
+#pragma unroll
+        for (int cy = 0; cy < 3; ++cy) {
+          const double f = wy[cy] * wz[cz];
+#pragma unroll
+          for (int cx = 0; cx < 3; ++cx) u[cx] += f * z1[cx + 3 * (cy + 3 * cz)];
+        }
+      const long long f0 = (long long)(iz * ey + iy) * ex;
+#pragma unroll
+      for (int x = 0; x < TLX; ++x) {
+        if (x >= ex) break;
+        double e = 0.0;
+#pragma unroll
+        for (int cx = 0; cx < 3; ++cx) e += wt(Wx, cx, c.cext[0], ex, x) * u[cx];
+        Yp[(f0 + x) * 32] = Xp[(f0 + x) * 32] + e;
+      }
+    }
+  }
+  // s = r - A y
+  for (int kz = 0; kz < ez; ++kz) {
+    const int iz = wk.fz ? ez - 1 - kz : kz;
+    for (int ky = 0; ky < ey; ++ky) {
+      const int iy = wk.fy ? ey - 1 - ky : ky;
+      double res[TLX];
+      tline_residual<false>(P, c, Yp, iy, iz, res);
+      const long long f0 = (long long)(iz * ey + iy) * ex;
+#pragma unroll
+      for (int x = 0; x < TLX; ++x) {
+        if (x >= ex) break;
+        __stcs(Sp + (f0 + x) * 32, res[x]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ smoothing phases
 // pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
 // post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
@@ -744,7 +917,13 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
     cudaFuncSetAttribute(k_vt_smooth<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_vt_smooth<3, false><<<wblocks, 32, smem, s>>>(P);
     LORPC_LAUNCHED();
-    k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
+    if (b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE")) {
+      // optional occupancy cap (shared-memory padding) for L2-locality studies
+      const int msm = getenv("LORPC_MID_SMEM") ? atoi(getenv("LORPC_MID_SMEM")) : 0;
+      if (msm > 0) cudaFuncSetAttribute(k_vt_mid3l, cudaFuncAttributeMaxDynamicSharedMemorySize, msm);
+      k_vt_mid3l<<<mblocks, 128, msm, s>>>(P);
+    }
+    else k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
     LORPC_LAUNCHED();
     k_vt_smooth<3, true><<<wblocks, 32, smem, s>>>(P);
   }
