@@ -535,7 +535,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   // (level-1 boxes of at most 3 (3D) / 5 (2D) nodes per axis, see vcycle_t.cu TCoarse)
   const int cext_max = (b->desc.patch_kind == 0 ? 2 : 3) * (lor->ml[1] - 1) - 1;
   b->tmode = b->Ld == 1 && b->max_n[1] <= 32 && cext_max <= (d == 3 ? 3 : 5) && tmode_smem(b) <= 227 * 1024 &&
-             b->max_n[0] <= 255;
+             b->max_n[0] <= 65534;
   if (const char* e = getenv("LORPC_TMODE")) b->tmode = b->tmode && atoi(e) != 0;
   if (b->tmode) LORPC_TRY(trec_build(b, s));
   return LORPC_OK;

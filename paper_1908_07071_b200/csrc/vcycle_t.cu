@@ -63,14 +63,17 @@ static std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
 // Padding entries carry L = 0 and the dummy node n0max, padding steps the dummy
 // node with count 0 (node indices are u8: thread mode requires n0max <= 254).
 struct TRecLayout { long long hdr, D, Lc, Ic, total; };
+// node index width of a warp's records: 1 byte when the largest patch has <= 254
+// nodes (C5, C2), else 2 bytes (C3)
+__host__ __device__ __forceinline__ int tiw(int n0max) { return n0max <= 254 ? 1 : 2; }
 __host__ __device__ __forceinline__ long long a256(long long b) { return (b + 255) & ~255ll; }
-__host__ __device__ __forceinline__ TRecLayout trec_layout(int S, int Kp) {
+__host__ __device__ __forceinline__ TRecLayout trec_layout(int S, int Kp, int iw) {
   TRecLayout T;
   T.hdr = 256;
   T.D = a256(T.hdr + 128ll * S);
   T.Lc = T.D + 256ll * S;
   T.Ic = T.Lc + 512ll * Kp;
-  T.total = a256(T.Ic + 64ll * Kp);
+  T.total = a256(T.Ic + 64ll * iw * Kp);
   return T;
 }
 
@@ -114,7 +117,8 @@ __global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, in
     const unsigned cb = t < n ? brp[t + 1] - brp[t] : 0u;
     Kp += tclass((int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2));
   }
-  const TRecLayout T = trec_layout(S, Kp);
+  const int iw = tiw(P.dummy);
+  const TRecLayout T = trec_layout(S, Kp, iw);
   if (!fill) {
     if (lane == 0) P.sizes[w] = T.total;
     return;
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, in
   uint32_t* H = (uint32_t*)(blk + T.hdr);
   double* Dd = (double*)(blk + T.D);
   double* Lc = (double*)(blk + T.Lc);
-  uint8_t* Ic = (uint8_t*)(blk + T.Ic);
+  char* Ic = blk + T.Ic;
   const double* Dn = (const double*)(rec + R.D);
   const double* bLv = (const double*)(rec + R.bL);
   const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
@@ -140,13 +144,14 @@ __global__ void __launch_bounds__(128) k_trec(TRecParams P, long long nslots, in
       dv = 1.0 / Dn[node];
     }
     const int mp = tclass((int)__reduce_max_sync(0xffffffffu, (cb + 1) / 2));
-    H[t * 32 + lane] = (uint32_t)node | (cb << 8) | ((uint32_t)mp << 16);
+    H[t * 32 + lane] = (uint32_t)node | (cb << 16) | ((uint32_t)mp << 24);
     Dd[t * 32 + lane] = dv;
     for (int k = 0; k < 2 * mp; ++k) {
       const bool in = k < (int)cb;
       const long long ix = ((long long)(kp + k / 2) * 32 + lane) * 2 + (k & 1);
       Lc[ix] = in ? bLv[b0 + k] : 0.0;
-      Ic[ix] = (uint8_t)(in ? bkv[b0 + k] : P.dummy);
+      const int nd = in ? bkv[b0 + k] : P.dummy;
+      if (iw == 1) ((uint8_t*)Ic)[ix] = (uint8_t)nd; else ((uint16_t*)Ic)[ix] = (uint16_t)nd;
     }
     kp += mp;
   }
@@ -291,41 +296,45 @@ struct TStage {
   double2 l[MP > 0 ? MP : 1];
   uint32_t c[MP > 0 ? MP : 1];
 };
-template <int MP>
-__device__ __forceinline__ void tload(TStage<MP>& g, const double2* __restrict__ Lp, const uint16_t* __restrict__ Cp,
+// index pairs: IW = 1: two u8 nodes in a u16; IW = 2: two u16 nodes in a u32
+template <int IW> __device__ __forceinline__ int ilo(uint32_t c) { return IW == 1 ? (c & 0xff) : (c & 0xffff); }
+template <int IW> __device__ __forceinline__ int ihi(uint32_t c) { return IW == 1 ? (c >> 8) : (c >> 16); }
+template <int MP, int IW>
+__device__ __forceinline__ void tload(TStage<MP>& g, const double2* __restrict__ Lp, const void* __restrict__ Cp,
                                       int kp) {
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
     g.l[p] = __ldcs(Lp + (long long)(kp + p) * 32);
-    g.c[p] = __ldcs(Cp + (long long)(kp + p) * 32);
+    if (IW == 1) g.c[p] = __ldcs((const uint16_t*)Cp + (long long)(kp + p) * 32);
+    else g.c[p] = __ldcs((const uint32_t*)Cp + (long long)(kp + p) * 32);
   }
 }
 // forward (push) step: yk = X[k]; X[i] -= L_ik yk over the column; X[k] = yk / D_k.
 // All neighbour values are loaded before any is stored (the nodes of a column are
 // distinct; padding entries carry L = 0 and the dummy node).
-template <int MP>
+template <int MP, int IW>
 __device__ __forceinline__ void tfwd_step(const TStage<MP>& g, uint32_t h, double dinv, double* X) {
-  const int k = h & 0xff;
+  const int k = h & 0xffff;
   const double yk = X[33 * k];
   double v0[MP > 0 ? MP : 1], v1[MP > 0 ? MP : 1];
 #pragma unroll
-  for (int p = 0; p < MP; ++p) { v0[p] = X[33 * (g.c[p] & 0xff)]; v1[p] = X[33 * (g.c[p] >> 8)]; }
+  for (int p = 0; p < MP; ++p) { v0[p] = X[33 * ilo<IW>(g.c[p])]; v1[p] = X[33 * ihi<IW>(g.c[p])]; }
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
-    X[33 * (g.c[p] & 0xff)] = v0[p] - g.l[p].x * yk;
-    X[33 * (g.c[p] >> 8)] = v1[p] - g.l[p].y * yk;
+    X[33 * ilo<IW>(g.c[p])] = v0[p] - g.l[p].x * yk;
+    X[33 * ihi<IW>(g.c[p])] = v1[p] - g.l[p].y * yk;
   }
   X[33 * k] = yk * dinv;
 }
 // backward (pull) step: X[k] -= sum_i L_ik X[i]; four partial sums
-template <int MP>
+template <int MP, int IW>
 __device__ __forceinline__ void tbwd_step(const TStage<MP>& g, uint32_t h, double* X) {
-  const int k = h & 0xff;
+  const int k = h & 0xffff;
   double a[4] = {X[33 * k], 0.0, 0.0, 0.0};
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
-    a[2 * (p & 1)] -= g.l[p].x * X[33 * (g.c[p] & 0xff)];
-    a[2 * (p & 1) + 1] -= g.l[p].y * X[33 * (g.c[p] >> 8)];
+    a[2 * (p & 1)] -= g.l[p].x * X[33 * ilo<IW>(g.c[p])];
+    a[2 * (p & 1) + 1] -= g.l[p].y * X[33 * ihi<IW>(g.c[p])];
   }
   X[33 * k] = (a[0] + a[1]) + (a[2] + a[3]);
 }
@@ -335,7 +344,8 @@ struct TSw {
   const uint32_t* H;    // header of step index 0 of the sweep order is H0; step s at H0 + s * dir
   const double* Dd;     // Dinv[t][lane] base
   const double2* Lp;    // pair rows [Kp][32] base
-  const uint16_t* Cp;
+  const char* Cp;       // index pair rows [Kp][32] (2 * iw bytes each), lane-adjusted
+  int iw;
   int S, Kp, s;         // steps, pair rows, current step (sweep order)
   int kp;               // forward: first pair row of step s; backward: one past its last
   uint32_t hc, hn;      // headers of steps s and s + 1 (0 past the end)
@@ -350,7 +360,7 @@ __device__ __forceinline__ void tprefetch(TSw& W, int kp) {
     while (W.pf < W.Kp && W.pf < kp + W.TPFD) {
       const int nr = min(8, W.Kp - W.pf);
       l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
-      l2_prefetch(W.Cp - W.lane + W.pf * 32, 64u * nr);
+      l2_prefetch(W.Cp + 2 * W.iw * (W.pf * 32 - W.lane), 64u * W.iw * nr);
       W.pf += nr;
     }
   } else {
@@ -358,16 +368,16 @@ __device__ __forceinline__ void tprefetch(TSw& W, int kp) {
       const int nr = min(8, W.pf);
       W.pf -= nr;
       l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
-      l2_prefetch(W.Cp - W.lane + W.pf * 32, 64u * nr);
+      l2_prefetch(W.Cp + 2 * W.iw * (W.pf * 32 - W.lane), 64u * W.iw * nr);
     }
   }
 }
-__device__ __forceinline__ int mpof(uint32_t h) { return (int)((h >> 16) & 0xffu); }
+__device__ __forceinline__ int mpof(uint32_t h) { return (int)(h >> 24); }
 
 // A run of consecutive steps of class MP, one step of software pipelining (the
 // next step's column is loaded while the current one is applied; the register
 // stages swap roles by the two-step unroll).  Returns at a class change or the end.
-template <int MP, bool BWD>
+template <int MP, bool BWD, int IW>
 __device__ __forceinline__ void trun(TSw& W, double* X) {
   const int dir = BWD ? -32 : 32;
   if constexpr (MP > 7) {
@@ -375,11 +385,11 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
     for (;;) {
       TStage<MP> A;
       const int kpA = BWD ? W.kp - MP : W.kp;
-      tload<MP>(A, W.Lp, W.Cp, kpA);
+      tload<MP, IW>(A, W.Lp, W.Cp, kpA);
       const double dA = BWD ? 1.0 : __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s));
       const uint32_t h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
       tprefetch<BWD>(W, kpA);
-      if (BWD) tbwd_step<MP>(A, W.hc, X); else tfwd_step<MP>(A, W.hc, dA, X);
+      if (BWD) tbwd_step<MP, IW>(A, W.hc, X); else tfwd_step<MP, IW>(A, W.hc, dA, X);
       W.s += 1; W.hc = W.hn; W.hn = h2;
       W.kp = BWD ? kpA : kpA + MP;
       if (!(W.s < W.S && mpof(W.hc) == MP)) return;
@@ -387,7 +397,7 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
   }
   TStage<MP> A, B;
   int kpA = BWD ? W.kp - MP : W.kp;
-  tload<MP>(A, W.Lp, W.Cp, kpA);
+  tload<MP, IW>(A, W.Lp, W.Cp, kpA);
   double dA = BWD ? 1.0 : __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s));
   for (;;) {
     // step s from A; B <- step s + 1 if it is of the same class
@@ -395,12 +405,12 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
     const int kpB = BWD ? kpA - MP : kpA + MP;
     double dB = 1.0;
     if (c1) {
-      tload<MP>(B, W.Lp, W.Cp, kpB);
+      tload<MP, IW>(B, W.Lp, W.Cp, kpB);
       if (!BWD) dB = __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s + 1));
     }
     uint32_t h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
     tprefetch<BWD>(W, kpA);
-    if (BWD) tbwd_step<MP>(A, W.hc, X); else tfwd_step<MP>(A, W.hc, dA, X);
+    if (BWD) tbwd_step<MP, IW>(A, W.hc, X); else tfwd_step<MP, IW>(A, W.hc, dA, X);
     W.s += 1; W.hc = W.hn; W.hn = h2;
     W.kp = BWD ? kpA : kpA + MP;
     if (!c1) return;
@@ -408,11 +418,11 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
     const bool c2 = W.s + 1 < W.S && mpof(W.hn) == MP;
     kpA = BWD ? kpB - MP : kpB + MP;
     if (c2) {
-      tload<MP>(A, W.Lp, W.Cp, kpA);
+      tload<MP, IW>(A, W.Lp, W.Cp, kpA);
       if (!BWD) dA = __ldg(W.Dd + 32 * tstep_t<BWD>(W, W.s + 1));
     }
     h2 = W.s + 2 < W.S ? __ldg(W.H + (W.s + 2) * dir) : 0u;
-    if (BWD) tbwd_step<MP>(B, W.hc, X); else tfwd_step<MP>(B, W.hc, dB, X);
+    if (BWD) tbwd_step<MP, IW>(B, W.hc, X); else tfwd_step<MP, IW>(B, W.hc, dB, X);
     W.s += 1; W.hc = W.hn; W.hn = h2;
     W.kp = BWD ? kpB : kpB + MP;
     if (!c2) return;
@@ -424,17 +434,18 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
 // dispatched once per run of equal step classes.  The record streams through L2
 // prefetches TPFD pair rows ahead.  X = the lane's column of the warp's shared
 // vectors; X[33 * dummy] must be zero on entry to the backward sweep.
-template <int NP, bool BWD>
+template <int NP, bool BWD, int IW>
 __device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
   const int4 hd = __ldg((const int4*)blk);
   TSw W;
   W.S = hd.x; W.Kp = hd.y;
   if (W.S == 0) return;
-  const TRecLayout T = trec_layout(W.S, W.Kp);
+  const TRecLayout T = trec_layout(W.S, W.Kp, IW);
+  W.iw = IW;
   W.H = (const uint32_t*)(blk + T.hdr) + lane + (BWD ? (W.S - 1) * 32 : 0);
   W.Dd = (const double*)(blk + T.D) + lane;
   W.Lp = (const double2*)(blk + T.Lc) + lane;
-  W.Cp = (const uint16_t*)(blk + T.Ic) + lane;
+  W.Cp = blk + T.Ic + 2 * IW * lane;
   W.TPFD = TPFD; W.lane = lane;
   W.pf = BWD ? W.Kp : 0;
   if (lane == 0) {
@@ -449,23 +460,23 @@ __device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, 
   tprefetch<BWD>(W, W.kp);
   while (W.s < W.S) {
     switch (mpof(W.hc)) {
-      case 0: trun<0, BWD>(W, X); break;
-      case 1: trun<1, BWD>(W, X); break;
-      case 2: trun<2, BWD>(W, X); break;
-      case 4: trun<4, BWD>(W, X); break;
-      case 7: if (NP >= 7) trun<(NP >= 7 ? 7 : 1), BWD>(W, X); break;
-      case 10: if (NP >= 10) trun<(NP >= 10 ? 10 : 1), BWD>(W, X); break;
-      default: if (NP >= 13) trun<(NP >= 13 ? 13 : 1), BWD>(W, X); break;
+      case 0: trun<0, BWD, IW>(W, X); break;
+      case 1: trun<1, BWD, IW>(W, X); break;
+      case 2: trun<2, BWD, IW>(W, X); break;
+      case 4: trun<4, BWD, IW>(W, X); break;
+      case 7: if (NP >= 7) trun<(NP >= 7 ? 7 : 1), BWD, IW>(W, X); break;
+      case 10: if (NP >= 10) trun<(NP >= 10 ? 10 : 1), BWD, IW>(W, X); break;
+      default: if (NP >= 13) trun<(NP >= 13 ? 13 : 1), BWD, IW>(W, X); break;
     }
   }
 }
 
 // M^{-1} applied in place to the lane's column X (forward, dummy reset, backward)
-template <int NP>
+template <int NP, int IW>
 __device__ __forceinline__ void tsmooth(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
-  tsweep<NP, false>(blk, X, TPFD, lane);
+  tsweep<NP, false, IW>(blk, X, TPFD, lane);
   X[33 * dummy] = 0.0;
-  tsweep<NP, true>(blk, X, TPFD, lane);
+  tsweep<NP, true, IW>(blk, X, TPFD, lane);
 }
 
 // ------------------------------------------------------------------ middle phase
@@ -822,7 +833,7 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
 // ------------------------------------------------------------------ smoothing phases
 // pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
 // post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
-template <int DIM, bool POST>
+template <int DIM, bool POST, int IW>
 __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   constexpr int NP = DIM == 3 ? 13 : 4;
   const int lane = threadIdx.x;
@@ -850,7 +861,7 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   }
   tsm[VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
-  tsmooth<NP>(blk, tsm + lane, n0, P.pfd, lane);
+  tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
   __syncwarp();
   if (!POST) {
     for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[VO(i, lane)]);
@@ -894,6 +905,23 @@ size_t tmode_smem(const lorpc_prec* b) {
   return (size_t)make_tparams(b, nullptr, nullptr).warp_doubles * sizeof(double);
 }
 
+template <int DIM, int IW>
+static int tlaunch(const TcParams& P, unsigned wblocks, unsigned mblocks, size_t smem, cudaStream_t s, bool lines) {
+  cudaFuncSetAttribute(k_vt_smooth<DIM, false, IW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_vt_smooth<DIM, true, IW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_vt_smooth<DIM, false, IW><<<wblocks, 32, smem, s>>>(P);
+  LORPC_LAUNCHED();
+  if constexpr (DIM == 3) {
+    if (lines) k_vt_mid3l<<<mblocks, 128, 0, s>>>(P);
+    else k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
+  } else {
+    k_vt_mid<2><<<mblocks, 128, 0, s>>>(P);
+  }
+  LORPC_LAUNCHED();
+  k_vt_smooth<DIM, true, IW><<<wblocks, 32, smem, s>>>(P);
+  return LORPC_OK;
+}
+
 int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
   const TcParams P = make_tparams(b, r, z);
   size_t smem = (size_t)P.warp_doubles * sizeof(double);
@@ -905,27 +933,12 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
   const unsigned wblocks = (unsigned)(P.nslots / 32), mblocks = (unsigned)((P.nslots + 127) / 128);
   if (b->m->d == 2) {
-    cudaFuncSetAttribute(k_vt_smooth<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_vt_smooth<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_vt_smooth<2, false><<<wblocks, 32, smem, s>>>(P);
-    LORPC_LAUNCHED();
-    k_vt_mid<2><<<mblocks, 128, 0, s>>>(P);
-    LORPC_LAUNCHED();
-    k_vt_smooth<2, true><<<wblocks, 32, smem, s>>>(P);
+    if (tiw(P.n0max) == 1) LORPC_TRY((tlaunch<2, 1>(P, wblocks, mblocks, smem, s, false)));
+    else LORPC_TRY((tlaunch<2, 2>(P, wblocks, mblocks, smem, s, false)));
   } else {
-    cudaFuncSetAttribute(k_vt_smooth<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_vt_smooth<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_vt_smooth<3, false><<<wblocks, 32, smem, s>>>(P);
-    LORPC_LAUNCHED();
-    if (b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE")) {
-      // optional occupancy cap (shared-memory padding) for L2-locality studies
-      const int msm = getenv("LORPC_MID_SMEM") ? atoi(getenv("LORPC_MID_SMEM")) : 0;
-      if (msm > 0) cudaFuncSetAttribute(k_vt_mid3l, cudaFuncAttributeMaxDynamicSharedMemorySize, msm);
-      k_vt_mid3l<<<mblocks, 128, msm, s>>>(P);
-    }
-    else k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
-    LORPC_LAUNCHED();
-    k_vt_smooth<3, true><<<wblocks, 32, smem, s>>>(P);
+    const bool lines = b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE");
+    if (tiw(P.n0max) == 1) LORPC_TRY((tlaunch<3, 1>(P, wblocks, mblocks, smem, s, lines)));
+    else LORPC_TRY((tlaunch<3, 2>(P, wblocks, mblocks, smem, s, lines)));
   }
   LORPC_LAUNCHED();
   return LORPC_OK;
