@@ -13,10 +13,12 @@ namespace lorpc {
 
 template <int DIM>
 __global__ void k_pre(const double* __restrict__ x, double* __restrict__ y, int3 N) {
-  const long long ndof = (long long)N.x * N.y * N.z;
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // 32-bit index arithmetic (grids below 2^31 nodes, checked by cg_apply)
+  const unsigned ndof = (unsigned)N.x * N.y * N.z;
+  const unsigned g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= ndof) return;
-  const int gx = (int)(g % N.x), gy = (int)((g / N.x) % N.y), gz = (int)(g / ((long long)N.x * N.y));
+  const unsigned gxy = g / (unsigned)N.x;
+  const int gx = (int)(g - gxy * N.x), gy = (int)(gxy % (unsigned)N.y), gz = (int)(gxy / (unsigned)N.y);
   bool d = gx == 0 || gx == N.x - 1 || gy == 0 || gy == N.y - 1;
   if (DIM == 3) d = d || gz == 0 || gz == N.z - 1;
   y[g] = d ? x[g] : 0.0;
@@ -224,6 +226,7 @@ static void launch2(const lorpc_mesh* m, const double* x, double* y, cudaStream_
 }
 
 int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
+  if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "cg_apply: grid of 2^31 nodes or more");
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   const unsigned g = (unsigned)((m->ndof_cg + 255) / 256);
   if (m->d == 2) k_pre<2><<<g, 256, 0, s>>>(x, y, N); else k_pre<3><<<g, 256, 0, s>>>(x, y, N);

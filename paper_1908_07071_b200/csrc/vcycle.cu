@@ -48,33 +48,39 @@ __global__ void k_restrict_vertex(const double* __restrict__ r, double* __restri
 template <int DIM>
 __global__ void k_prolong_vertex_add(const double* __restrict__ zc, double* __restrict__ z, int3 nv, int3 N, int3 n,
                                      Basis1D bs) {
-  const long long NT = (long long)N.x * N.y * N.z;
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // 32-bit index arithmetic (grids below 2^31 nodes, checked by the caller)
+  const unsigned NT = (unsigned)N.x * N.y * N.z;
+  const unsigned g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= NT) return;
-  const int gc[3] = {(int)(g % N.x), (int)((g / N.x) % N.y), (int)(g / ((long long)N.x * N.y))};
+  const unsigned gxy = g / (unsigned)N.x;
+  const int gc[3] = {(int)(g - gxy * N.x), (int)(gxy % (unsigned)N.y), (int)(gxy / (unsigned)N.y)};
   const int Nn[3] = {N.x, N.y, N.z}, nn[3] = {n.x, n.y, n.z};
   bool dir = false;
+#pragma unroll
   for (int k = 0; k < DIM; ++k) if (gc[k] == 0 || gc[k] == Nn[k] - 1) dir = true;
   if (dir) { z[g] = 0.0; return; }
   const int p = bs.p;
   int v0[3] = {0, 0, 0};
   double w0[3] = {1, 1, 1}, w1[3] = {0, 0, 0};
+#pragma unroll
   for (int k = 0; k < DIM; ++k) {
     const int e = min(gc[k] / p, nn[k] - 1);
     const int a = gc[k] - e * p;
-    v0[k] = e; w0[k] = 1.0 - bs.xi[a]; w1[k] = bs.xi[a];
+    v0[k] = e; w1[k] = bs.xi[a]; w0[k] = 1.0 - w1[k];
   }
   double acc = 0.0;
+  const unsigned vb = v0[0] + (unsigned)nv.x * (v0[1] + (unsigned)nv.y * v0[2]);
+#pragma unroll
   for (int sel = 0; sel < (1 << DIM); ++sel) {
     double w = 1.0;
-    int vv[3] = {0, 0, 0};
+    unsigned off = 0;
+#pragma unroll
     for (int k = 0; k < DIM; ++k) {
       const int b = (sel >> k) & 1;
       w *= b ? w1[k] : w0[k];
-      vv[k] = v0[k] + b;
+      if (b) off += k == 0 ? 1u : (k == 1 ? (unsigned)nv.x : (unsigned)nv.x * nv.y);
     }
-    if (w == 0.0) continue;
-    acc += w * zc[vv[0] + (long long)nv.x * (vv[1] + (long long)nv.y * vv[2])];
+    acc += w * __ldg(zc + vb + off);  // w = 0 terms read an existing vertex (clamped element)
   }
   z[g] += acc;
 }
@@ -542,6 +548,7 @@ static int gmg_vcycle_t(const lorpc_prec* b, const double** out, cudaStream_t s)
 int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStream_t s) {
   int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, m->d == 3 ? m->n[2] + 1 : 1);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]), n = make_int3(m->n[0], m->n[1], m->n[2]);
+  if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "prolong_vertex_add: grid of 2^31 nodes or more");
   if (m->d == 2) k_prolong_vertex_add<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
   else k_prolong_vertex_add<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
   LORPC_LAUNCHED();
@@ -561,6 +568,7 @@ static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStr
   LORPC_LAUNCHED();
   const double* z0 = nullptr;
   LORPC_TRY(gmg_vcycle_t<DIM>(b, &z0, s));
+  if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "coarse_apply: grid of 2^31 nodes or more");
   k_prolong_vertex_add<DIM><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z0, z, nv, N, n, m->basis);
   LORPC_LAUNCHED();
   return LORPC_OK;
