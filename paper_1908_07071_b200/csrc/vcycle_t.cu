@@ -286,9 +286,14 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 }
 
 // Shared-memory layout of the warp's 32 patch vectors: node i of patch (lane) q
-// at word 33 i + q, conflict-free for lanes = patches at one node and for lanes =
-// consecutive nodes of one patch.  X points at the lane's column (word q).
-#define VO(i, q) ((i) * 33 + (q))
+// at word 32 i + q: the sweeps (lanes = patches, each at its own node) are
+// conflict-free for any node indices (lane q always hits bank pair q mod 16); the
+// gather / scatter phases therefore also run lane = patch.  X points at the
+// lane's column (word q).
+#ifndef LORPC_XS
+#define LORPC_XS 32
+#endif
+#define VO(i, q) ((i) * LORPC_XS + (q))
 
 // One step's column data in registers: MP pair rows (compile-time class size)
 template <int MP>
@@ -315,28 +320,28 @@ __device__ __forceinline__ void tload(TStage<MP>& g, const double2* __restrict__
 template <int MP, int IW>
 __device__ __forceinline__ void tfwd_step(const TStage<MP>& g, uint32_t h, double dinv, double* X) {
   const int k = h & 0xffff;
-  const double yk = X[33 * k];
+  const double yk = X[LORPC_XS * k];
   double v0[MP > 0 ? MP : 1], v1[MP > 0 ? MP : 1];
 #pragma unroll
-  for (int p = 0; p < MP; ++p) { v0[p] = X[33 * ilo<IW>(g.c[p])]; v1[p] = X[33 * ihi<IW>(g.c[p])]; }
+  for (int p = 0; p < MP; ++p) { v0[p] = X[LORPC_XS * ilo<IW>(g.c[p])]; v1[p] = X[LORPC_XS * ihi<IW>(g.c[p])]; }
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
-    X[33 * ilo<IW>(g.c[p])] = v0[p] - g.l[p].x * yk;
-    X[33 * ihi<IW>(g.c[p])] = v1[p] - g.l[p].y * yk;
+    X[LORPC_XS * ilo<IW>(g.c[p])] = v0[p] - g.l[p].x * yk;
+    X[LORPC_XS * ihi<IW>(g.c[p])] = v1[p] - g.l[p].y * yk;
   }
-  X[33 * k] = yk * dinv;
+  X[LORPC_XS * k] = yk * dinv;
 }
 // backward (pull) step: X[k] -= sum_i L_ik X[i]; four partial sums
 template <int MP, int IW>
 __device__ __forceinline__ void tbwd_step(const TStage<MP>& g, uint32_t h, double* X) {
   const int k = h & 0xffff;
-  double a[4] = {X[33 * k], 0.0, 0.0, 0.0};
+  double a[4] = {X[LORPC_XS * k], 0.0, 0.0, 0.0};
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
-    a[2 * (p & 1)] -= g.l[p].x * X[33 * ilo<IW>(g.c[p])];
-    a[2 * (p & 1) + 1] -= g.l[p].y * X[33 * ihi<IW>(g.c[p])];
+    a[2 * (p & 1)] -= g.l[p].x * X[LORPC_XS * ilo<IW>(g.c[p])];
+    a[2 * (p & 1) + 1] -= g.l[p].y * X[LORPC_XS * ihi<IW>(g.c[p])];
   }
-  X[33 * k] = (a[0] + a[1]) + (a[2] + a[3]);
+  X[LORPC_XS * k] = (a[0] + a[1]) + (a[2] + a[3]);
 }
 
 // Sweep cursor over a T-record block (lane-adjusted pointers)
@@ -433,7 +438,7 @@ __device__ __forceinline__ void trun(TSw& W, double* X) {
 // (push, steps ascending, diagonal fused) or backward (pull, steps descending),
 // dispatched once per run of equal step classes.  The record streams through L2
 // prefetches TPFD pair rows ahead.  X = the lane's column of the warp's shared
-// vectors; X[33 * dummy] must be zero on entry to the backward sweep.
+// vectors; X[LORPC_XS * dummy] must be zero on entry to the backward sweep.
 template <int NP, bool BWD, int IW>
 __device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
   const int4 hd = __ldg((const int4*)blk);
@@ -475,7 +480,7 @@ __device__ __forceinline__ void tsweep(const char* __restrict__ blk, double* X, 
 template <int NP, int IW>
 __device__ __forceinline__ void tsmooth(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
   tsweep<NP, false, IW>(blk, X, TPFD, lane);
-  X[33 * dummy] = 0.0;
+  X[LORPC_XS * dummy] = 0.0;
   tsweep<NP, true, IW>(blk, X, TPFD, lane);
 }
 
@@ -842,20 +847,24 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   const int nq = (int)min(32ll, P.J - w * 32);
   const char* blk = P.trec + P.trecoff[w];
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-  TPatch* tpa = (TPatch*)(tsm + P.tpoff);
-  if (lane < nq) tpa[lane] = tpatch<DIM>(P.G, P.pord[w * 32 + lane]);
+  // gather / scatter lane = patch: with the unpadded layout (stride LORPC_XS = 32)
+  // lanes = patches at one node are conflict-free, and the lanes' nodes of
+  // x-consecutive patches are p apart in r / z
+  TPatch c{};
+  float rex = 1.0f, rexy = 1.0f;
+  if (lane < nq) {
+    c = tpatch<DIM>(P.G, P.pord[w * 32 + lane]);
+    rex = 1.0f / c.ext[0]; rexy = 1.0f / (c.ext[0] * c.ext[1]);
+  }
+  auto gidx = [&](int i) {
+    int ix, iy, iz;
+    box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
+    return (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0));
+  };
   const long long col = w * (long long)n0 * 32 + lane;
   if (!POST) {
-    __syncwarp();
-    for (int q = 0; q < nq; ++q) {  // r_j = I_j^T r (a5)
-      const TPatch c = tpa[q];
-      const float rex = 1.0f / c.ext[0], rexy = 1.0f / (c.ext[0] * c.ext[1]);
-      for (int i = lane; i < c.n; i += 32) {
-        int ix, iy, iz;
-        box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
-        tsm[VO(i, q)] = __ldg(P.r + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)));
-      }
-    }
+    for (int i = 0; i < n0; ++i)  // r_j = I_j^T r (a5)
+      tsm[VO(i, lane)] = (lane < nq && i < c.n) ? __ldg(P.r + gidx(i)) : 0.0;
   } else {
     for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] = __ldcs(P.spark + col + i * 32);
   }
@@ -867,17 +876,8 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
     for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[VO(i, lane)]);
   } else {
     for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] += __ldcs(P.ypark + col + i * 32);  // z_j = y + M^{-1} s
-    __syncwarp();
-    for (int q = 0; q < nq; ++q) {  // z += I_j z_j (a8), lanes over consecutive nodes
-      const TPatch c = tpa[q];
-      const float rex = 1.0f / c.ext[0], rexy = 1.0f / (c.ext[0] * c.ext[1]);
-      for (int i = lane; i < c.n; i += 32) {
-        int ix, iy, iz;
-        box_xyz(i, c.ext[0], c.ext[1], rex, rexy, ix, iy, iz);
-        atomicAdd(P.z + (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (DIM == 3 ? c.lo[2] + iz : 0)),
-                  tsm[VO(i, q)]);
-      }
-    }
+    if (lane < nq)
+      for (int i = 0; i < c.n; ++i) atomicAdd(P.z + gidx(i), tsm[VO(i, lane)]);  // z += I_j z_j (a8)
   }
 }
 
