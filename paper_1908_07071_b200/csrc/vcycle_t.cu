@@ -274,7 +274,6 @@ struct TcParams {
   const double* Cp;  // [warps][NPK][32] packed dense coarse operators
   double *xpark, *ypark, *spark;  // [warp][n0max][32] x, y, s of the warp's patches (lane columns)
   int n0max;         // largest finest-level patch (= the dummy node index)
-  int tpoff;         // the warp's 32 patch geometries (TPatch)
   int pfd;           // L2 prefetch distance of the sweeps (pair rows)
   int warp_doubles;
   const double* r;
@@ -895,7 +894,6 @@ static TcParams make_tparams(const lorpc_prec* b, const double* r, double* z) {
   P.xpark = b->zpark; P.ypark = b->zpark + pcol; P.spark = b->zpark + 2 * pcol;
   P.r = r; P.z = z;
   int acc = VO(b->max_n[0] + 1, 0);
-  P.tpoff = acc; acc += 32 * (int)(sizeof(TPatch) / sizeof(double));
   P.warp_doubles = (acc + 1) & ~1;
   P.pfd = getenv("LORPC_TPFD") ? atoi(getenv("LORPC_TPFD")) : 32;
   return P;
@@ -907,8 +905,11 @@ size_t tmode_smem(const lorpc_prec* b) {
 
 template <int DIM, int IW>
 static int tlaunch(const TcParams& P, unsigned wblocks, unsigned mblocks, size_t smem, cudaStream_t s, bool lines) {
+  // the whole shared-memory carveout: C5's 32.3 KB of vectors per warp then fit 7 warps per SM
   cudaFuncSetAttribute(k_vt_smooth<DIM, false, IW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_vt_smooth<DIM, true, IW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_vt_smooth<DIM, false, IW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_vt_smooth<DIM, true, IW>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   k_vt_smooth<DIM, false, IW><<<wblocks, 32, smem, s>>>(P);
   LORPC_LAUNCHED();
   if constexpr (DIM == 3) {
