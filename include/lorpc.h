@@ -149,7 +149,10 @@ int lorpc_prec_profile_read(lorpc_prec* b, double* ms, long long* launches);
 
 /* ---- PCG (a10) ------------------------------------------------------------------ */
 /* Preconditioned conjugate gradients (reading c12): x_0 = 0,
- * stop when ||r_k||_2 <= rtol ||b||_2.  x_dev is overwritten.  Device-resident
+ * stop when ||r_k||_2 <= rtol ||b||_2.  CG: b's Dirichlet entries must be zero
+ * (homogeneous Dirichlet, as lorpc_rhs_assemble writes them; B has zero rows there,
+ * so a nonzero b_D cannot be reduced and the solve ends in NOT_CONVERGED or
+ * BREAKDOWN).  x_dev is overwritten.  Device-resident
  * vectors; synchronizes the stream.  Returns LORPC_ERR_NOT_CONVERGED or
  * LORPC_ERR_BREAKDOWN with the report filled up to the last iteration. */
 int lorpc_pcg_solve(const lorpc_mesh* m, const lorpc_prec* b, const double* b_dev, double* x_dev,
