@@ -205,6 +205,9 @@ void lorpc_dist_destroy(lorpc_dist* d);
 /* Local rank `local` (0 in NCCL mode; 0..nranks-1 in emulation): global index of
  * its first owned node, owned node count, patch count. */
 int lorpc_dist_info(const lorpc_dist* d, int local, long long* owned_offset, long long* n_owned, long long* n_patches);
+/* The rank's local patch preconditioner (owned vertex-plane patches, no coarse
+ * term; owned by d): for lorpc_prec_info / lorpc_prec_bytes (byte model). */
+int lorpc_dist_local_prec(const lorpc_dist* d, int local, const lorpc_prec** out);
 /* y = A x and z = B r on the distributed vectors: arrays of one device pointer per
  * local rank, each the rank's owned range [owned_offset, owned_offset + n_owned)
  * of the global vector.  Asynchronous on the creation stream. */

@@ -469,6 +469,12 @@ int lorpc_dist_info(const lorpc_dist* D, int local, long long* owned_offset, lon
   return LORPC_OK;
 }
 
+int lorpc_dist_local_prec(const lorpc_dist* D, int local, const lorpc_prec** out) {
+  if (!D || !out || local < 0 || local >= D->nlocal) return fail(LORPC_ERR_ARG, "dist_local_prec: bad argument");
+  *out = D->R[local].prec;
+  return LORPC_OK;
+}
+
 int lorpc_dist_operator_apply(lorpc_dist* D, const double* const* x_owned, double* const* y_owned) {
   if (!D || !x_owned || !y_owned) return fail(LORPC_ERR_ARG, "dist_operator_apply: NULL");
   for (int i = 0; i < D->nlocal; ++i)

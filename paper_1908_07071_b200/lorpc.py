@@ -47,7 +47,7 @@ SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc
            "lorpc_prec_profile_read", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
            "lorpc_launch_count", "lorpc_last_error",
            "lorpc_dist_plan_get", "lorpc_dist_nccl_id", "lorpc_dist_create", "lorpc_dist_destroy",
-           "lorpc_dist_info", "lorpc_dist_operator_apply", "lorpc_dist_precond_apply", "lorpc_dist_pcg_solve"]
+           "lorpc_dist_info", "lorpc_dist_local_prec", "lorpc_dist_operator_apply", "lorpc_dist_precond_apply", "lorpc_dist_pcg_solve"]
 
 
 class DistPlan(ctypes.Structure):
@@ -90,6 +90,7 @@ def lib():
                                         _vp, ctypes.POINTER(_vp)]
         L.lorpc_dist_destroy.argtypes = [_vp]
         L.lorpc_dist_info.argtypes = [_vp, _int, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
+        L.lorpc_dist_local_prec.argtypes = [_vp, _int, ctypes.POINTER(_vp)]
         L.lorpc_dist_operator_apply.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
         L.lorpc_dist_precond_apply.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
         L.lorpc_dist_pcg_solve.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _d, _int,
@@ -300,6 +301,17 @@ class Dist:
     @staticmethod
     def _ptrs(ts):
         return (_vp * len(ts))(*[_dptr(t) for t in ts])
+
+    def local_byte_model(self, local=0):
+        """(factor values, [local level-grid nodes]) of the rank's patch preconditioner."""
+        h = _vp()
+        _check(lib().lorpc_dist_local_prec(self.h, int(local), ctypes.byref(h)))
+        J, Lv = _ll(), _int()
+        _check(lib().lorpc_prec_info(h, ctypes.byref(J), ctypes.byref(Lv)))
+        fv, cn = _ll(), _ll()
+        ln = (_ll * 8)()
+        _check(lib().lorpc_prec_bytes(h, ctypes.byref(fv), ln, ctypes.byref(cn)))
+        return fv.value, [ln[i] for i in range(Lv.value)]
 
     def apply(self, xs, ys):
         _check(lib().lorpc_dist_operator_apply(self.h, self._ptrs(xs), self._ptrs(ys)))
