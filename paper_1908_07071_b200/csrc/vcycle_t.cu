@@ -216,7 +216,7 @@ __global__ void k_pack_c(const double* __restrict__ Cd, double* __restrict__ Cp,
 
 int trec_build(lorpc_prec* b, cudaStream_t s) {
   const long long nw = (b->J + 31) / 32, nslots = nw * 32;
-  int TX = 32, TY = 8;
+  int TX = 32, TY = 32;  // measured on C5 (r01): 32 x 32 < 32 x 16 < 32 x 8 < lexicographic in V-cycle time
   if (const char* e = getenv("LORPC_TILE")) {  // "0": lexicographic order; "TXxTY" otherwise
     if (atoi(e) == 0) TX = TY = 1 << 30;
     else sscanf(e, "%dx%d", &TX, &TY);
