@@ -30,7 +30,8 @@ def rel(a, b):
 
 
 # C5 recipe (trilinear, perturbed, random RHS) on small meshes; ranks up to n_z
-CASES = [((4, 3, 5), 3, 2), ((4, 3, 5), 3, 5), ((3, 4, 7), 3, 3), ((3, 3, 6), 4, 2), ((3, 3, 4), 2, 4)]
+CASES = [((4, 3, 5), 3, 2), ((4, 3, 5), 3, 5), ((3, 4, 7), 3, 3), ((3, 3, 6), 4, 2), ((3, 3, 4), 2, 4),
+         ((4, 3, 8), 3, 8)]  # eight ranks of one element layer each (the 8-GPU C5 shape in miniature)
 
 
 def split(D, v):
