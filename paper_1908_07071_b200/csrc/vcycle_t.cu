@@ -289,6 +289,9 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 // conflict-free for any node indices (lane q always hits bank pair q mod 16); the
 // gather / scatter phases therefore also run lane = patch.  X points at the
 // lane's column (word q).
+#ifndef LORPC_PFR
+#define LORPC_PFR 8  // pair rows per L2 bulk prefetch
+#endif
 #ifndef LORPC_XS
 #define LORPC_XS 32
 #endif
@@ -362,14 +365,14 @@ __device__ __forceinline__ void tprefetch(TSw& W, int kp) {
   if (W.lane != 0) return;
   if (!BWD) {
     while (W.pf < W.Kp && W.pf < kp + W.TPFD) {
-      const int nr = min(8, W.Kp - W.pf);
+      const int nr = min(LORPC_PFR, W.Kp - W.pf);
       l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
       l2_prefetch(W.Cp + 2 * W.iw * (W.pf * 32 - W.lane), 64u * W.iw * nr);
       W.pf += nr;
     }
   } else {
     while (W.pf > 0 && W.pf > kp - W.TPFD) {
-      const int nr = min(8, W.pf);
+      const int nr = min(LORPC_PFR, W.pf);
       W.pf -= nr;
       l2_prefetch(W.Lp - W.lane + W.pf * 32, 512u * nr);
       l2_prefetch(W.Cp + 2 * W.iw * (W.pf * 32 - W.lane), 64u * W.iw * nr);
