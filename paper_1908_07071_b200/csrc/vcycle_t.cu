@@ -289,6 +289,9 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 // conflict-free for any node indices (lane q always hits bank pair q mod 16); the
 // gather / scatter phases therefore also run lane = patch.  X points at the
 // lane's column (word q).
+#ifndef LORPC_RLD
+#define LORPC_RLD __ldcs  // T-record loads (streaming)
+#endif
 #ifndef LORPC_PFR
 #define LORPC_PFR 8  // pair rows per L2 bulk prefetch
 #endif
@@ -311,9 +314,9 @@ __device__ __forceinline__ void tload(TStage<MP>& g, const double2* __restrict__
                                       int kp) {
 #pragma unroll
   for (int p = 0; p < MP; ++p) {
-    g.l[p] = __ldcs(Lp + (long long)(kp + p) * 32);
-    if (IW == 1) g.c[p] = __ldcs((const uint16_t*)Cp + (long long)(kp + p) * 32);
-    else g.c[p] = __ldcs((const uint32_t*)Cp + (long long)(kp + p) * 32);
+    g.l[p] = LORPC_RLD(Lp + (long long)(kp + p) * 32);
+    if (IW == 1) g.c[p] = LORPC_RLD((const uint16_t*)Cp + (long long)(kp + p) * 32);
+    else g.c[p] = LORPC_RLD((const uint32_t*)Cp + (long long)(kp + p) * 32);
   }
 }
 // forward (push) step: yk = X[k]; X[i] -= L_ik yk over the column; X[k] = yk / D_k.
