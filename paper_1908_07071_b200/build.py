@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "liblorpc.so")
-SOURCES = ["basis.cpp", "mesh.cu", "operator.cu", "lor.cu", "schwarz.cu", "vcycle.cu", "vcycle_t.cu", "pcg.cu", "dg.cu", "dist.cu", "api.cu"]
+SOURCES = ["basis.cpp", "mesh.cu", "operator.cu", "lor.cu", "schwarz.cu", "vcycle.cu", "vcycle_t.cu", "vcycle_w.cu", "pcg.cu", "dg.cu", "dist.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr"] + \

@@ -181,6 +181,7 @@ int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void
 void lorpc_prec_destroy(lorpc_prec* b) {
   if (!b) return;
   dfree(b->rec); dfree(b->recoff); dfree(b->trec); dfree(b->trecoff); dfree(b->zpark); dfree(b->Cdi); dfree(b->pord);
+  dfree(b->wrec); dfree(b->wrecoff); dfree(b->Cq);
   for (int i = 0; i < MAXC; ++i) {
     if (i > 0) dfree(b->Ac[i]);
     dfree(b->dl1[i]); dfree(b->cr[i]); dfree(b->cz[i]); dfree(b->cs[i]);

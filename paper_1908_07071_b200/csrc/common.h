@@ -129,6 +129,15 @@ struct lorpc_prec {
   double* zpark = nullptr;          // per-warp r_1 / z_1 scratch
   double* Cdi = nullptr;            // dense coarse operators, packed symmetric, interleaved by patch per warp
   int* pord = nullptr;
+  // warp-per-patch fused V-cycle (vcycle_w.cu): shared-memory-staged W-records
+  bool wmode = false;
+  char* wrec = nullptr;
+  long long* wrecoff = nullptr;     // [wslots + 1] byte offsets, slot order
+  long long wrec_bytes = 0;
+  int wrec_max = 0;                 // largest W-record (bytes)
+  long long wslots = 0;
+  double* Cq = nullptr;             // [wslots][378] packed dense coarse operators
+  int wlp = 16;                     // lanes per patch of the W kernel (16: two patches per warp)
   // coarse space (R_0)
   int nc = 0;                       // GMG levels
   int cn[lorpc::MAXC][3];           // vertices per axis

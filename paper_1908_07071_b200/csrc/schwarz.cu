@@ -31,6 +31,8 @@ Transfer1D gmg_transfer();
 int dense_coarse_setup(lorpc_prec* b, cudaStream_t s);  // vcycle.cu
 int trec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_t.cu
 size_t tmode_smem(const lorpc_prec* b);
+int wrec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_w.cu
+size_t wmode_smem(const lorpc_prec* b);
 
 // ------------------------------------------------------------------ MDF + ILU(0)
 __device__ __forceinline__ double q30(double x) {
@@ -531,6 +533,22 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   LORPC_TRY(dalloc(&b->Cd, (size_t)b->J * b->ldc));
   LORPC_TRY(dense_coarse_setup(b, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
+  // warp-per-patch fused V-cycle (vcycle_w.cu): 3D vertex patches with a level-1 box
+  // of at most 3 x 3 x 3 nodes (p = 3) and node indices that fit in a byte
+  {
+    const int cx = 2 * (lor->ml[1] - 1) - 1;
+    // opt-in (LORPC_WMODE=1): parity-exact, but measured slower than the thread-mode
+    // kernels on C5: only ~14 patches fit per SM with their factor
+    // resident, and the push-round chains are latency-bound
+    const bool eligible = d == 3 && b->desc.patch_kind == 0 && b->Ld == 1 && cx <= 3 && b->max_n[0] <= 255;
+    const char* e = getenv("LORPC_WMODE");
+    b->wmode = eligible && e && atoi(e) != 0;
+    if (b->wmode) {
+      LORPC_TRY(wrec_build(b, s));
+      if (wmode_smem(b) > 227 * 1024) return fail(LORPC_ERR_SIZE, "wmode: record does not fit in shared memory");
+      return LORPC_OK;
+    }
+  }
   // thread-per-patch V-cycle when the warp's 32 patch vectors fit in shared memory
   // (level-1 boxes of at most 3 (3D) / 5 (2D) nodes per axis, see vcycle_t.cu TCoarse)
   const int cext_max = (b->desc.patch_kind == 0 ? 2 : 3) * (lor->ml[1] - 1) - 1;

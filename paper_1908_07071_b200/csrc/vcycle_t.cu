@@ -30,7 +30,7 @@ namespace lorpc {
 // run at nearly the same time and meet in L2: z-neighbours are one tile layer
 // (TX * TY patches) apart, while lexicographic order puts them a whole patch plane
 // apart, beyond the L2 reuse window of the concurrently resident warps.
-static std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
+std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
   const lorpc_mesh* m = b->m;
   const int d = m->d, star = b->desc.patch_kind == 1;
   const int gx = m->n[0] + (star ? 0 : 1), gy = m->n[1] + (star ? 0 : 1);

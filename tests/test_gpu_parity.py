@@ -321,3 +321,30 @@ def test_full_size_c5_preconditioner_and_pcg(L):
     P.schwarz_setup("vertex", "mdf", "gmg")
     _, ro = P.pcg(random_free_rhs(small), small.tol)
     assert abs(rep["iters"] - ro["iters"]) <= 3, (rep["iters"], ro["iters"])
+
+
+# ---------------------------------------------------------------- W-mode V-cycle (opt-in kernel)
+@pytest.mark.parametrize("lp", ["16", "32"])
+@pytest.mark.parametrize("name", ["C5s", "C3p2"])
+def test_wmode_precond_and_pcg_parity(L, name, lp, monkeypatch):
+    """The warp-per-patch fused V-cycle (vcycle_w.cu, LORPC_WMODE=1): element-wise
+    preconditioner parity and PCG iterations +-1 against the oracle."""
+    monkeypatch.setenv("LORPC_WMODE", "1")
+    monkeypatch.setenv("LORPC_WLP", lp)
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg)
+    r = parity_vector(P.ndof, seed=43)
+    X = P.node_coords()
+    free = np.all((X > 1e-12) & (X < 1 - 1e-12), axis=1)
+    r[~free] = 0.0
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    zo = P.precond(r)
+    zg = z.cpu().numpy()
+    assert rel(zg, zo) <= TOL
+    assert np.abs(zg - zo).max() <= TOL * np.abs(zo).max()
+    bo = random_free_rhs(cfg) if cfg.rhs == "randn" else P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty_like(z)
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, cfg.tol)
+    _, ro = P.pcg(bo, cfg.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 1
