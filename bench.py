@@ -147,7 +147,7 @@ def run_lorpc(args):
     import numpy as np
     import torch
     from paper_1908_07071_b200 import build as B
-    from workloads import get_config, random_free_rhs, rhs_function, vertices
+    from workloads import get_config
 
     rank, world, local = dist_env()
     if not os.path.exists(os.path.join(ROOT, "paper_1908_07071_b200", "liblorpc.so")):
@@ -168,25 +168,18 @@ def run_lorpc(args):
     if world > 1 or force_dist:
         return run_lorpc_dist(args, cfg, dev, rank, world, dist)
     t0 = time.perf_counter()
-    mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, vertices(cfg))
-    lor = L.Lor(mesh)
-    prec = L.Prec(lor, patch_kind=cfg.patch_kind)
-    if cfg.rhs == "randn":
-        b_host = random_free_rhs(cfg)
-        b = torch.from_numpy(b_host).to(dev)
-    else:
-        xq = torch.empty(mesh.n_quad * cfg.dim, dtype=torch.float64, device=dev)
-        mesh.quad_points(xq)
-        fq = torch.from_numpy(rhs_function(cfg, xq.cpu().numpy().reshape(-1, cfg.dim))).to(dev)
-        b = torch.empty(mesh.n_dof, dtype=torch.float64, device=dev)
-        mesh.rhs_assemble(fq, None, b)
-        b_host = b.cpu().numpy()
-    x = torch.empty_like(b)
+    probs = build_problems(L, cfg, dev)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
 
+    def step():
+        its = []
+        for pr in probs:
+            its.append(L.pcg_solve(pr["mesh"], pr["prec"], pr["b"], pr["x"], cfg.tol, cfg.maxit)["iters"])
+        return its
+
     for _ in range(args.warmup):
-        L.pcg_solve(mesh, prec, b, x, cfg.tol, cfg.maxit)
+        step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -194,19 +187,21 @@ def run_lorpc(args):
     clocks = Clocks(local)
     clocks.start()
     L.launch_count(reset=True)
-    prec.profile(True)
+    for pr in probs:
+        pr["prec"].profile(True)
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = []
     e0.record(s)
     for _ in range(args.steps):
-        rep = L.pcg_solve(mesh, prec, b, x, cfg.tol, cfg.maxit)
-        iters.append(rep["iters"])
+        iters.append(step())
     e1.record(s)
     torch.cuda.synchronize()
     launches = L.launch_count()
-    vc_ms, vc_n = prec.profile_read()
-    prec.profile(False)
+    vc = []
+    for pr in probs:
+        vc.append(pr["prec"].profile_read())
+        pr["prec"].profile(False)
     ck = clocks.stop()
     ms = e0.elapsed_time(e1)
     if dist:
@@ -214,69 +209,145 @@ def run_lorpc(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
         dist.barrier()
-    work = mesh.n_dof * sum(iters) * world
+    n_dof = probs[0]["mesh"].n_dof
+    work = n_dof * sum(sum(it) for it in iters) * world
     value = work / (ms * 1e-3)
 
     # end to end: host (pinned) b in, host x out, through lorpc_pcg_solve_host
-    bh = torch.from_numpy(b_host).pin_memory()
-    xh = torch.empty(mesh.n_dof, dtype=torch.float64).pin_memory()
+    for pr in probs:
+        pr["bh"] = torch.from_numpy(pr["b_host"]).pin_memory()
+        pr["xh"] = torch.empty(n_dof, dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
     te = time.perf_counter()
     it_e2e = 0
     for _ in range(args.steps):
-        rep = L.pcg_solve_host(mesh, prec, bh.numpy(), xh.numpy(), cfg.tol, cfg.maxit)
-        it_e2e += rep["iters"]
+        for pr in probs:
+            rep = L.pcg_solve_host(pr["mesh"], pr["prec"], pr["bh"].numpy(), pr["xh"].numpy(), cfg.tol, cfg.maxit)
+            it_e2e += rep["iters"]
     torch.cuda.synchronize()
     te = time.perf_counter() - te
     if dist:
         tt = torch.tensor([te], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
-    e2e = mesh.n_dof * it_e2e * world / te
+    e2e = n_dof * it_e2e * world / te
+
+    # operator apply (a2 / a3): CUDA events around repeated applies of the solve vectors
+    pr0 = probs[0]
+    y = torch.empty_like(pr0["x"])
+    for _ in range(3):
+        pr0["mesh"].apply(pr0["x"], y)
+    oa, ob = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_op = 20
+    oa.record(s)
+    for _ in range(n_op):
+        pr0["mesh"].apply(pr0["x"], y)
+    ob.record(s)
+    torch.cuda.synchronize()
+    op_ms = oa.elapsed_time(ob) / n_op
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
-    # roofline of the dominant kernel: patch V-cycle (algorithmic bytes, DESIGN.md §Roofline)
-    fv, lvl_nodes, cnodes = prec.byte_model()
-    half = 14 if cfg.dim == 3 else 5
-    vc_bytes = 8 * fv + 8 * half * sum(lvl_nodes) + 16 * mesh.n_dof
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
+    # roofline of the dominant kernel: patch V-cycle (algorithmic bytes, DESIGN.md §Roofline)
+    prec0 = pr0["prec"]
+    fv, lvl_nodes, cnodes = prec0.byte_model()
+    half = 14 if cfg.dim == 3 else 5
+    n_cg = lvl_nodes[0]
+    vc_bytes = 8 * fv + 8 * half * sum(lvl_nodes) + 16 * n_cg
+    vc_ms = sum(v[0] for v in vc)
+    vc_n = sum(v[1] for v in vc)
     per_launch_ms = vc_ms / max(vc_n, 1)
     achieved = vc_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("k_vcycle_bytes_per_launch")
+    working_set = vc_bytes + 40 * n_dof
+    # operator algorithmic bytes: x + y, plus the per-point geometric factors when the
+    # geometry is not affine (C2, C5); affine meshes need one G per element
+    nel = 1
+    for v in cfg.n:
+        nel *= v
+    q = cfg.p + 1
+    ncomp = cfg.dim * (cfg.dim + 1) // 2
+    g_bytes = 8 * ncomp * q ** cfg.dim * nel if cfg.perturb > 0 else 0
+    op_bytes = 16 * n_dof + g_bytes
+    op_ach = op_bytes / (op_ms * 1e-3) / 1e9
+    disc = "SIPG" if cfg.disc == "sipg" else "CG"
+    pens = f", eta=(p+1)^2*{{{','.join(str(c) for c in cfg.penalty_c)}}} (one solve each per step), weak BC" \
+        if cfg.disc == "sipg" else ""
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded workloads/ generators)",
-            "config": {"workload": f"{cfg.name}: {cfg.dim}D {cfg.disc.upper()} {'x'.join(map(str, cfg.n))} "
+            "config": {"workload": f"{cfg.name}: {cfg.dim}D {disc} {'x'.join(map(str, cfg.n))} "
                                    f"p={cfg.p}, perturb={cfg.perturb}h, {cfg.patch_kind} patches, "
-                                   f"MDF-ILU(0) V(1,1), GMG R_0, tol={cfg.tol}",
-                       "n_dof": mesh.n_dof, "pcg_iters_per_solve": iters[0], "n_patches": prec.n_patches,
+                                   f"MDF-ILU(0) V(1,1), GMG R_0{pens}, tol={cfg.tol}",
+                       "n_dof": n_dof, "pcg_iters_per_solve": iters[0], "n_patches": prec0.n_patches,
                        "setup_s": round(t_setup, 3), "parallelism": "replicas" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (working set >> 126 MB)" if mesh.n_dof > 4_000_000
-                       else "L2-resident working set (no flush; latency case)"},
+                       "l2": "inputs larger than L2 (working set >> 126 MB)" if working_set > 4 * 126e6
+                       else "L2-resident working set (no flush; latency case)",
+                       "working_set_bytes": working_set},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "patch V-cycle apply (k_vt_smooth pre + k_vt_mid + k_vt_smooth post)",
+                         "kernel": prec0.kernel(),
                          "algorithmic_bytes_per_launch": vc_bytes, "launch_ms": per_launch_ms,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * mesh.n_dof,
-                    "d2h_bytes_per_step": 8 * mesh.n_dof},
+            "roofline_operator": {"bound": "hbm" if g_bytes else "fp64", "achieved": op_ach, "peak": peak,
+                                  "unit": "GB/s", "frac": op_ach / peak,
+                                  "kernel": "SIPG volume + face kernels (k_dgvol3, k_dgface3)" if cfg.disc == "sipg"
+                                  else f"sum-factorised operator (k_cg{cfg.dim})",
+                                  "algorithmic_bytes_per_launch": op_bytes, "launch_ms": op_ms,
+                                  "note": "x + y (16 B/dof) + per-point G when non-affine; CUDA events over "
+                                          f"{n_op} applies after the timed region"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n_dof * len(probs),
+                    "d2h_bytes_per_step": 8 * n_dof * len(probs)},
             "gpu_launches": launches, "clocks": ck}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE:
         cb, _ = oracle_sample(args.config)
         line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def build_problems(L, cfg, dev):
+    """The config's solves: one for CG configs, one per penalty for SIPG (C4)."""
+    import torch
+    from workloads import dirichlet_function, random_free_rhs, rhs_function, vertices
+    V = vertices(cfg)
+    pens = [(cfg.p + 1) ** 2 * c for c in cfg.penalty_c] if cfg.disc == "sipg" else [None]
+    out = []
+    for eta in pens:
+        if eta is None:
+            mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, V)
+        else:
+            mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, V, disc=1, eta=eta)
+        lor = L.Lor(mesh)
+        prec = L.Prec(lor, patch_kind=cfg.patch_kind)
+        if cfg.rhs == "randn":
+            b_host = random_free_rhs(cfg)
+            b = torch.from_numpy(b_host).to(dev)
+        else:
+            xq = torch.empty(mesh.n_quad * cfg.dim, dtype=torch.float64, device=dev)
+            xb = torch.empty(max(mesh.n_bface_quad, 1) * cfg.dim, dtype=torch.float64, device=dev) \
+                if eta is not None else None
+            mesh.quad_points(xq, xb)
+            fq = torch.from_numpy(rhs_function(cfg, xq.cpu().numpy().reshape(-1, cfg.dim))).to(dev)
+            gq = torch.from_numpy(dirichlet_function(cfg, xb.cpu().numpy().reshape(-1, cfg.dim))).to(dev) \
+                if eta is not None else None
+            b = torch.empty(mesh.n_dof, dtype=torch.float64, device=dev)
+            mesh.rhs_assemble(fq, gq, b)
+            b_host = b.cpu().numpy()
+        out.append({"mesh": mesh, "lor": lor, "prec": prec, "b": b, "b_host": b_host, "x": torch.empty_like(b),
+                    "eta": eta})
+    return out
 
 
 def run_lorpc_dist(args, cfg, dev, rank, world, dist):

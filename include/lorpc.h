@@ -43,7 +43,9 @@ typedef enum {
   LORPC_ERR_BREAKDOWN = 5,        /* PCG p.Ap <= 0 or r.z <= 0 (iteration in message) */
   LORPC_ERR_NOT_CONVERGED = 6,    /* PCG hit maxit */
   LORPC_ERR_CUDA = 7,             /* CUDA runtime error */
-  LORPC_ERR_OOM = 8               /* device allocation failed */
+  LORPC_ERR_OOM = 8,              /* device allocation failed */
+  LORPC_ERR_NOT_SPD = 9,          /* a matrix that must be SPD is not (coarsest R_0 level: Cholesky pivot <= 0) */
+  LORPC_ERR_NCCL = 10             /* NCCL error in the multi-GPU path (lorpc_dist_*) */
 } lorpc_status;
 
 typedef struct lorpc_mesh lorpc_mesh;
@@ -135,6 +137,12 @@ int lorpc_precond_apply(const lorpc_prec* b, const double* r_dev, double* z_dev,
 int lorpc_prec_export_ordering(const lorpc_prec* b, long long patch, int level, int* perm_host, int* n);
 /* Number of patches and hierarchy levels. */
 int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels);
+/* Which patch V-cycle kernel family lorpc_precond_apply runs (a5-a8; for bench
+ * labels): 0 = group mode (k_vcycle: VG lanes per patch, every level in shared
+ * memory), 1 = thread mode (vcycle_t.cu: one lane per patch, warp-interleaved
+ * factors), 2 = W mode (vcycle_w.cu: warp-per-patch fused V-cycle, opt-in through
+ * LORPC_WMODE=1).  Errors: LORPC_ERR_ARG on NULL. */
+int lorpc_prec_kernel(const lorpc_prec* b, int* mode);
 /* Algorithmic byte-model inputs: factor_values = sum over
  * patches and levels of (free nodes + stencil edges), i.e. the L and D values of
  * every M_l = L D L^T; level_nodes[l] = nodes of the level-l grid (l < n_levels),

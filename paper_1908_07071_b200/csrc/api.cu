@@ -1,4 +1,5 @@
 // C ABI (include/lorpc.h): argument checking, handle lifetime, dispatch.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -9,11 +10,15 @@ const char* last_error();
 int apply_operator(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s);
 int export_ordering(const lorpc_prec* b, long long j, int l, int* perm, int* n);
 
-int apply_precond(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
-  if (b->m->desc.disc == 0) return schwarz_apply_cg(b, r, z, s);
+int apply_precond(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart) {
+  if (b->m->desc.disc == 0) return schwarz_apply_cg(b, r, z, s, rzpart);
   LORPC_TRY(dg_restrict_cg(b->m, r, b->rcg, s));
   LORPC_TRY(schwarz_apply_cg(b, b->rcg, b->zcg, s));
   return dg_combine(b->m, r, b->zcg, z, s);
+}
+// r.z can ride on the last pass over z (the coarse prolongation) for CG with R_0
+long long rz_parts(const lorpc_prec* b) {
+  return (b->m->desc.disc == 0 && b->desc.coarse == 0) ? (b->m->ndof_cg + 255) / 256 : 0;
 }
 }  // namespace lorpc
 
@@ -168,11 +173,16 @@ int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void
   if (rc == LORPC_OK) rc = dalloc(&b->pv, (size_t)m->ndof);
   if (rc == LORPC_OK) rc = dalloc(&b->qv, (size_t)m->ndof);
   if (rc == LORPC_OK) rc = dalloc(&b->scal, 16);
-  if (rc == LORPC_OK) rc = dalloc(&b->part, 1024);
+  b->npart = std::max<long long>(1024, rz_parts(b));
+  if (rc == LORPC_OK) rc = dalloc(&b->part, (size_t)b->npart);
   if (rc == LORPC_OK && cudaMallocHost(&b->hostpin, 16 * sizeof(double)) != cudaSuccess)
     rc = fail(LORPC_ERR_OOM, "cudaMallocHost");
-  if (rc == LORPC_OK && (cudaEventCreate(&b->ev0) != cudaSuccess || cudaEventCreate(&b->ev1) != cudaSuccess))
+  if (rc == LORPC_OK && (cudaEventCreate(&b->ev0) != cudaSuccess || cudaEventCreate(&b->ev1) != cudaSuccess ||
+                         cudaEventCreateWithFlags(&b->evf, cudaEventDisableTiming) != cudaSuccess ||
+                         cudaEventCreateWithFlags(&b->evj, cudaEventDisableTiming) != cudaSuccess))
     rc = fail(LORPC_ERR_CUDA, "cudaEventCreate");
+  if (rc == LORPC_OK && cudaStreamCreateWithFlags(&b->aux, cudaStreamNonBlocking) != cudaSuccess)
+    rc = fail(LORPC_ERR_CUDA, "cudaStreamCreate");
   if (rc != LORPC_OK) { lorpc_prec_destroy(b); return rc; }
   *out = b;
   return LORPC_OK;
@@ -186,11 +196,14 @@ void lorpc_prec_destroy(lorpc_prec* b) {
     if (i > 0) dfree(b->Ac[i]);
     dfree(b->dl1[i]); dfree(b->cr[i]); dfree(b->cz[i]); dfree(b->cs[i]);
   }
-  dfree(b->coarse_chol); dfree(b->rcg); dfree(b->zcg); dfree(b->xb); dfree(b->wtab); dfree(b->Cd);
+  dfree(b->coarse_chol); dfree(b->coarse_idx); dfree(b->rcg); dfree(b->zcg); dfree(b->xb); dfree(b->wtab); dfree(b->Cd);
   dfree(b->r); dfree(b->z); dfree(b->pv); dfree(b->qv); dfree(b->scal); dfree(b->part);
   if (b->hostpin) cudaFreeHost(b->hostpin);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
+  if (b->evf) cudaEventDestroy(b->evf);
+  if (b->evj) cudaEventDestroy(b->evj);
+  if (b->aux) cudaStreamDestroy(b->aux);
   for (auto& e : b->prof_ev) cudaEventDestroy(e);
   delete b;
 }
@@ -198,7 +211,7 @@ void lorpc_prec_destroy(lorpc_prec* b) {
 int lorpc_precond_apply(const lorpc_prec* b, const double* r_dev, double* z_dev, void* stream) {
   if (!b || !r_dev || !z_dev) return fail(LORPC_ERR_ARG, "precond_apply: NULL argument");
   if (r_dev == z_dev) return fail(LORPC_ERR_ARG, "precond_apply: r and z alias");
-  return apply_precond(b, r_dev, z_dev, S(stream));
+  return apply_precond(b, r_dev, z_dev, S(stream), nullptr);
 }
 
 int lorpc_prec_export_ordering(const lorpc_prec* b, long long patch, int level, int* perm_host, int* n) {
@@ -210,6 +223,12 @@ int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels) {
   if (!b) return fail(LORPC_ERR_ARG, "prec_info: NULL");
   if (n_patches) *n_patches = b->J;
   if (n_levels) *n_levels = b->L;
+  return LORPC_OK;
+}
+
+int lorpc_prec_kernel(const lorpc_prec* b, int* mode) {
+  if (!b || !mode) return fail(LORPC_ERR_ARG, "prec_kernel: NULL");
+  *mode = b->wmode ? 2 : b->tmode ? 1 : 0;
   return LORPC_OK;
 }
 
@@ -262,9 +281,12 @@ int lorpc_pcg_solve(const lorpc_mesh* m, const lorpc_prec* b, const double* b_de
 int lorpc_pcg_solve_host(const lorpc_mesh* m, const lorpc_prec* b, const double* b_host, double* x_host, double rtol,
                          int maxit, lorpc_pcg_report* rep, void* stream) {
   if (!m || !b || !b_host || !x_host || !rep) return fail(LORPC_ERR_ARG, "pcg_solve_host: NULL argument");
+  if (b->m != m) return fail(LORPC_ERR_ARG, "pcg_solve_host: preconditioner built for another mesh");
+  if (!(rtol > 0.0) || maxit < 1) return fail(LORPC_ERR_ARG, "pcg_solve_host: rtol > 0 and maxit >= 1 required");
   cudaStream_t s = S(stream);
   lorpc_prec* bb = const_cast<lorpc_prec*>(b);
-  if (!bb->xb) LORPC_TRY(dalloc(&bb->xb, (size_t)2 * m->ndof));
+  if (bb->xb && bb->xb_n != m->ndof) { dfree(bb->xb); bb->xb_n = 0; }
+  if (!bb->xb) { LORPC_TRY(dalloc(&bb->xb, (size_t)2 * m->ndof)); bb->xb_n = m->ndof; }
   double* bd = bb->xb;
   double* xd = bb->xb + m->ndof;
   LORPC_CUDA(cudaMemcpyAsync(bd, b_host, sizeof(double) * m->ndof, cudaMemcpyHostToDevice, s));

@@ -147,7 +147,8 @@ struct lorpc_prec {
   double* cr[lorpc::MAXC];
   double* cz[lorpc::MAXC];
   double* cs[lorpc::MAXC];
-  double* coarse_chol = nullptr;    // dense LDL^T of the coarsest GMG level
+  double* coarse_chol = nullptr;    // dense inverse of the coarsest GMG level's interior matrix
+  int* coarse_idx = nullptr;        // its interior vertices (grid indices)
   int ncoarsest = 0;
   // DG workspace
   double* rcg = nullptr;
@@ -158,8 +159,11 @@ struct lorpc_prec {
   double* part = nullptr;           // reduction partials
   double* hostpin = nullptr;        // pinned scalars
   double* xb = nullptr;             // host-buffer solve staging (b, x)
-  cudaStream_t aux = nullptr;       // second stream (coarse chain)
+  long long xb_n = 0;               // length the staging buffer was sized for
+  cudaStream_t aux = nullptr;       // second stream (R_0 chain, concurrent with the patch batch)
+  cudaEvent_t evf = nullptr, evj = nullptr;  // fork / join of the aux stream
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long long npart = 0;              // capacity of part (reduction partials)
   // live timing of the dominant kernel (patch V-cycle), lorpc_prec_profile()
   bool prof_on = false;
   int prof_n = 0;
@@ -182,7 +186,8 @@ int gmg_build(lorpc_prec* b, double* Ac0, const int* nv, int d, cudaStream_t s);
 int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
 int gmg_vcycle(const lorpc_prec* b, const double** out, cudaStream_t s);
 int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStream_t s);
-int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
+int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart = nullptr);
+long long rz_parts(const lorpc_prec* b);  // blocks of the fused r.z partial sums (0: not fused)
 int quad_points(const lorpc_mesh* m, double* xq, double* xbq, cudaStream_t s);
 int rhs_assemble(const lorpc_mesh* m, const double* fq, const double* gq, double* b, cudaStream_t s);
 int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double* x, double rtol,

@@ -162,7 +162,7 @@ struct lorpc_dist {
 namespace {
 
 int nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) return fail(LORPC_ERR_CUDA, std::string(what) + ": " + ncclGetErrorString(r));
+  if (r != ncclSuccess) return fail(LORPC_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
   return LORPC_OK;
 }
 #define LORPC_NCCL(call) LORPC_TRY(nccl_check((call), #call))
@@ -231,9 +231,15 @@ int exchange(lorpc_dist* D, int k, double* DistRank::*v) {
   if (cnt == 0) return LORPC_OK;
   double* rbuf = add ? R.tmp : R.*v + R.plan.recv0[k] * pl;
   LORPC_NCCL(ncclGroupStart());
-  if (R.plan.to[k] >= 0) LORPC_NCCL(ncclSend(R.*v + R.plan.send0[k] * pl, (size_t)cnt, ncclDouble, R.plan.to[k], D->comm, D->s));
-  if (R.plan.from[k] >= 0) LORPC_NCCL(ncclRecv(rbuf, (size_t)cnt, ncclDouble, R.plan.from[k], D->comm, D->s));
-  LORPC_NCCL(ncclGroupEnd());
+  // the group is closed before any error is returned (an open group would leave the
+  // communicator unusable)
+  ncclResult_t e1 = ncclSuccess, e2 = ncclSuccess;
+  if (R.plan.to[k] >= 0) e1 = ncclSend(R.*v + R.plan.send0[k] * pl, (size_t)cnt, ncclDouble, R.plan.to[k], D->comm, D->s);
+  if (e1 == ncclSuccess && R.plan.from[k] >= 0) e2 = ncclRecv(rbuf, (size_t)cnt, ncclDouble, R.plan.from[k], D->comm, D->s);
+  const ncclResult_t e3 = ncclGroupEnd();
+  LORPC_NCCL(e1);
+  LORPC_NCCL(e2);
+  LORPC_NCCL(e3);
   if (add && R.plan.from[k] >= 0) {
     k_add_planes_free<<<nb(cnt, 256), 256, 0, D->s>>>(R.*v + R.plan.recv0[k] * pl, rbuf, Nx, Ny, cnt);
     LORPC_LAUNCHED();
@@ -332,7 +338,7 @@ void lorpc_dist_destroy(lorpc_dist* D) {
     lorpc_prec* c = D->coarse;
     for (int l = 1; l < c->nc; ++l) dfree(c->Ac[l]);
     for (int l = 0; l < c->nc; ++l) { dfree(c->dl1[l]); dfree(c->cr[l]); dfree(c->cz[l]); dfree(c->cs[l]); }
-    dfree(c->coarse_chol);
+    dfree(c->coarse_chol); dfree(c->coarse_idx);
     delete c;
   }
   delete D->cmesh;

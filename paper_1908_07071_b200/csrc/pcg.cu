@@ -3,8 +3,13 @@
 // x_0 = 0, r_0 = b, z = B r, p = z, rho = r.z; per iteration: q = A p,
 // alpha = rho / p.q, x += alpha p, r -= alpha q, stop if ||r|| <= rtol ||b||,
 // z = B r, rho' = r.z, beta = rho'/rho, p = z + beta p.
-// Scalars stay on the device; dot products are deterministic two-stage
-// reductions (fixed grid, fixed tree); the host reads ||r|| once per iteration.
+// Scalars stay on the device; the dot products are two-stage reductions with a fixed
+// grid and tree (deterministic for a given z; the atomics of the operator and patch
+// scatters make z itself order-dependent in the last bits).  rho = r.z is fused into
+// the last pass over z (the coarse prolongation) when B has its R_0 term; the R_0
+// chain itself runs on a second stream concurrently with the patch batch
+// (vcycle.cu).  On p.Ap <= 0 alpha is set to 0, so a BREAKDOWN return leaves x and r
+// as they were.  The host reads ||r|| once per iteration.
 #include <cmath>
 
 #include "device.cuh"
@@ -42,7 +47,7 @@ __global__ void k_dot_final(const double* __restrict__ part, int np, double* sca
   if (threadIdx.x == 0) {
     switch (mode) {
       case 0: scal[S_RHO] = s; break;
-      case 1: scal[S_PQ] = s; scal[S_ALPHA] = scal[S_RHO] / s; break;
+      case 1: scal[S_PQ] = s; scal[S_ALPHA] = s > 0.0 ? scal[S_RHO] / s : 0.0; break;
       case 2: scal[S_RR] = s; break;
       case 3: scal[S_RZ] = s; scal[S_BETA] = s / scal[S_RHO]; scal[S_RHO] = s; break;
       case 4: scal[S_BB] = s; break;
@@ -83,7 +88,21 @@ static int dot(const double* a, const double* b, long long n, double* part, doub
 int apply_operator(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
   return m->desc.disc == 0 ? cg_apply(m, x, y, s) : dg_apply(m, x, y, s);
 }
-int apply_precond(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);
+int apply_precond(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart);
+
+// z = B r and rho = r.z (mode 0: rho_0; mode 3: beta, rho)
+static int precond_rho(const lorpc_prec* b, const double* r, double* z, long long n, double* part, double* scal,
+                       int mode, cudaStream_t s) {
+  const long long np = rz_parts(b);
+  if (np > 0) {
+    LORPC_TRY(apply_precond(b, r, z, s, part));
+    k_dot_final<<<1, 1024, 0, s>>>(part, (int)np, scal, mode);
+    LORPC_LAUNCHED();
+    return LORPC_OK;
+  }
+  LORPC_TRY(apply_precond(b, r, z, s, nullptr));
+  return dot(r, z, n, part, scal, mode, s);
+}
 
 int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double* x, double rtol, int maxit,
             lorpc_pcg_report* rep, cudaStream_t s) {
@@ -109,9 +128,8 @@ int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double
     LORPC_CUDA(cudaEventRecord(b->ev1, s));
     return LORPC_OK;
   }
-  LORPC_TRY(apply_precond(b, r, z, s));
+  LORPC_TRY(precond_rho(b, r, z, n, part, scal, 0, s));
   LORPC_CUDA(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-  LORPC_TRY(dot(r, z, n, part, scal, 0, s));
   int status = LORPC_ERR_NOT_CONVERGED;
   for (int k = 1; k <= maxit; ++k) {
     LORPC_TRY(apply_operator(m, p, q, s));
@@ -133,8 +151,7 @@ int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double
     rep->rel_res = rel;
     if (rep->res_hist) rep->res_hist[k] = rel;
     if (rel <= rtol) { rep->converged = 1; status = LORPC_OK; break; }
-    LORPC_TRY(apply_precond(b, r, z, s));
-    LORPC_TRY(dot(r, z, n, part, scal, 3, s));
+    LORPC_TRY(precond_rho(b, r, z, n, part, scal, 3, s));
     k_update_p<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, z, n, scal);
     LORPC_LAUNCHED();
   }

@@ -18,6 +18,7 @@
 // weights, exact LDL^T at the coarsest level (reading c8); the patch result is
 // added into z with atomics (a8).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -305,42 +306,6 @@ __global__ void k_l1diag(const double* __restrict__ A, double* __restrict__ dl, 
 
 // GMG smoothing kernels on a vertex grid (interior nodes; boundary nodes hold 0)
 
-template <int DIM>
-__global__ void k_coarsest_factor(const double* __restrict__ A, double* __restrict__ F, int3 Nv, int nint) {
-  constexpr int ND = Dirs<DIM>::ND;
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
-  // interior index map
-  int idx = 0;
-  for (long long g = 0; g < NT; ++g) {
-    int c[3];
-    if (!interior_of<DIM>(g, Nv, c)) continue;
-    for (int j = 0; j < nint; ++j) F[idx * nint + j] = 0.0;
-    for (int d = 0; d < ND; ++d) {
-      const long long h = g + dir_dx(d) + (long long)Nv.x * (dir_dy(d) + (long long)Nv.y * (DIM == 3 ? dir_dz(d) : 0));
-      int cc[3];
-      if (h < 0 || h >= NT || !interior_of<DIM>(h, Nv, cc)) continue;
-      // interior rank of h
-      int rk = 0;
-      for (long long t = 0; t < h; ++t) { int c2[3]; if (interior_of<DIM>(t, Nv, c2)) ++rk; }
-      F[idx * nint + rk] = A[g * Dirs<DIM>::NDP + d];
-    }
-    ++idx;
-  }
-  // in-place Cholesky (lower)
-  for (int j = 0; j < nint; ++j) {
-    double s = F[j * nint + j];
-    for (int k = 0; k < j; ++k) s -= F[j * nint + k] * F[j * nint + k];
-    const double c = sqrt(s);
-    F[j * nint + j] = c;
-    for (int i = j + 1; i < nint; ++i) {
-      double t = F[i * nint + j];
-      for (int k = 0; k < j; ++k) t -= F[i * nint + k] * F[j * nint + k];
-      F[i * nint + j] = t / c;
-    }
-  }
-}
-
 // ------------------------------------------------------------------ setup driver
 PatchGeom make_geom(const lorpc_prec* b) {
   PatchGeom G{};
@@ -356,7 +321,8 @@ PatchGeom make_geom(const lorpc_prec* b) {
 
 // R_0 hierarchy on a vertex grid nv (reading c11): level 0 operator Ac0 (full
 // stencil, node-major; not owned), 2:1 Galerkin coarsening while every axis has
-// an even number (> 2) of intervals, dense Cholesky of the coarsest interior.
+// an even number (> 2) of intervals, exact solve on the coarsest interior (any
+// size up to 2048 vertices: odd or anisotropic grids stop coarsening early).
 int gmg_build(lorpc_prec* b, double* Ac0, const int* nv, int d, cudaStream_t s) {
   b->nc = 0;
   for (int i = 0; i < MAXC; ++i) { b->Ac[i] = b->dl1[i] = b->cr[i] = b->cz[i] = b->cs[i] = nullptr; }
@@ -388,15 +354,75 @@ int gmg_build(lorpc_prec* b, double* Ac0, const int* nv, int d, cudaStream_t s) 
     ++lvl;
   }
   b->nc = lvl + 1;
-  int nint = 1;
-  for (int k = 0; k < d; ++k) nint *= b->cn[lvl][k] - 2;
-  if (nint > 64) return fail(LORPC_ERR_SIZE, "coarsest GMG level too large");
+  // coarsest level: exact solve (reading c11) through the dense inverse of its interior
+  // matrix, formed once here on the host (Cholesky, then L^{-T} L^{-1}); the apply is
+  // a parallel dense matvec (k_coarsest_inv)
+  const int3 nvl = i3(b->cn[lvl]);
+  const long long NT = b->cN[lvl];
+  std::vector<int> ilist;
+  for (long long g = 0; g < NT; ++g) {
+    const int c[3] = {(int)(g % nvl.x), (int)((g / nvl.x) % nvl.y), (int)(g / ((long long)nvl.x * nvl.y))};
+    bool in = c[0] > 0 && c[0] < nvl.x - 1 && c[1] > 0 && c[1] < nvl.y - 1;
+    if (d == 3) in = in && c[2] > 0 && c[2] < nvl.z - 1;
+    if (in) ilist.push_back((int)g);
+  }
+  const int nint = (int)ilist.size();
+  if (nint > 2048)
+    return fail(LORPC_ERR_SIZE, "coarsest GMG level has " + std::to_string(nint) +
+                                    " interior vertices (> 2048): the vertex grid does not halve evenly enough");
   b->ncoarsest = nint;
   LORPC_TRY(dalloc(&b->coarse_chol, (size_t)std::max(nint * nint, 1)));
+  LORPC_TRY(dalloc(&b->coarse_idx, (size_t)std::max(nint, 1)));
   if (nint > 0) {
-    if (d == 2) k_coarsest_factor<2><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
-    else k_coarsest_factor<3><<<1, 1, 0, s>>>(b->Ac[lvl], b->coarse_chol, i3(b->cn[lvl]), nint);
-    LORPC_LAUNCHED();
+    const int ndp = ndp_of(d), ND = d == 2 ? 9 : 27;
+    std::vector<double> A((size_t)NT * ndp);
+    LORPC_CUDA(cudaMemcpyAsync(A.data(), b->Ac[lvl], sizeof(double) * A.size(), cudaMemcpyDeviceToHost, s));
+    LORPC_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> rank((size_t)NT, -1);
+    for (int i = 0; i < nint; ++i) rank[ilist[i]] = i;
+    std::vector<double> F((size_t)nint * nint, 0.0);
+    for (int i = 0; i < nint; ++i) {
+      const long long g = ilist[i];
+      for (int dd = 0; dd < ND; ++dd) {
+        const long long h = g + dir_dx(dd) + (long long)nvl.x * (dir_dy(dd) + (long long)nvl.y * (d == 3 ? dir_dz(dd) : 0));
+        if (h < 0 || h >= NT || rank[h] < 0) continue;
+        F[(size_t)i * nint + rank[h]] = A[(size_t)g * ndp + dd];
+      }
+    }
+    // Cholesky F = C C^T (lower, in place)
+    for (int j = 0; j < nint; ++j) {
+      double sj = F[(size_t)j * nint + j];
+      for (int k = 0; k < j; ++k) sj -= F[(size_t)j * nint + k] * F[(size_t)j * nint + k];
+      if (!(sj > 0.0)) return fail(LORPC_ERR_NOT_SPD, "coarsest GMG level: matrix not positive definite");
+      const double cj = std::sqrt(sj);
+      F[(size_t)j * nint + j] = cj;
+      for (int i = j + 1; i < nint; ++i) {
+        double t = F[(size_t)i * nint + j];
+        for (int k = 0; k < j; ++k) t -= F[(size_t)i * nint + k] * F[(size_t)j * nint + k];
+        F[(size_t)i * nint + j] = t / cj;
+      }
+    }
+    // W = C^{-1} (lower), then inv = W^T W
+    std::vector<double> W((size_t)nint * nint, 0.0);
+    for (int j = 0; j < nint; ++j) {
+      W[(size_t)j * nint + j] = 1.0 / F[(size_t)j * nint + j];
+      for (int i = j + 1; i < nint; ++i) {
+        double t = 0.0;
+        for (int k = j; k < i; ++k) t += F[(size_t)i * nint + k] * W[(size_t)k * nint + j];
+        W[(size_t)i * nint + j] = -t / F[(size_t)i * nint + i];
+      }
+    }
+    std::vector<double> Inv((size_t)nint * nint, 0.0);
+    for (int i = 0; i < nint; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double t = 0.0;
+        for (int k = i; k < nint; ++k) t += W[(size_t)k * nint + i] * W[(size_t)k * nint + j];
+        Inv[(size_t)i * nint + j] = t;
+        Inv[(size_t)j * nint + i] = t;
+      }
+    LORPC_CUDA(cudaMemcpyAsync(b->coarse_chol, Inv.data(), sizeof(double) * Inv.size(), cudaMemcpyHostToDevice, s));
+    LORPC_CUDA(cudaMemcpyAsync(b->coarse_idx, ilist.data(), sizeof(int) * ilist.size(), cudaMemcpyHostToDevice, s));
+    LORPC_CUDA(cudaStreamSynchronize(s));
   }
   return LORPC_OK;
 }
@@ -428,6 +454,8 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
       patch_box(G, j, l, lo, ext);
       const int n = std::max(ext[0] * ext[1] * ext[2], 0);
       if (n > 65535) return fail(LORPC_ERR_SIZE, "patch too large");
+      if (num_edges(d, ext) > 65535)  // record row offsets (frp / brp) are u16
+        return fail(LORPC_ERR_SIZE, "patch has more than 65535 stencil edges");
       b->max_n[l] = std::max(b->max_n[l], n);
       b->recoff_h[j * L + l] = off;
       const long long nL = num_edges(d, ext);

@@ -45,20 +45,45 @@ __global__ void k_restrict_vertex(const double* __restrict__ r, double* __restri
 }
 
 // z += P_0 z_0, then z_D = 0
+// With rdot != nullptr the kernel also leaves per-block partial sums of r . z (the
+// final z) in part[blockIdx.x]: PCG's rho = r.z fused into the last pass over z.
+__device__ __forceinline__ double block_sum256(double v) {
+  __shared__ double sh[8];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = threadIdx.x < 8 ? sh[threadIdx.x] : 0.0;
+  if (w == 0) v = warp_sum(v);
+  return v;
+}
 template <int DIM>
-__global__ void k_prolong_vertex_add(const double* __restrict__ zc, double* __restrict__ z, int3 nv, int3 N, int3 n,
-                                     Basis1D bs) {
-  // 32-bit index arithmetic (grids below 2^31 nodes, checked by the caller)
+__device__ __forceinline__ double prolong_vertex_node(const double* __restrict__ zc, double* __restrict__ z, int3 nv,
+                                                      int3 N, int3 n, const Basis1D& bs, unsigned g);
+template <int DIM>
+__global__ void __launch_bounds__(256) k_prolong_vertex_add(const double* __restrict__ zc, double* __restrict__ z, int3 nv,
+                                                           int3 N, int3 n, Basis1D bs, const double* __restrict__ rdot,
+                                                           double* __restrict__ part) {
   const unsigned NT = (unsigned)N.x * N.y * N.z;
   const unsigned g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= NT) return;
+  const double zg = g < NT ? prolong_vertex_node<DIM>(zc, z, nv, N, n, bs, g) : 0.0;
+  if (rdot) {
+    const double t = block_sum256(g < NT ? rdot[g] * zg : 0.0);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+  }
+}
+// z[g] += (P_0 zc)[g], z_D = 0; returns the new z[g]
+template <int DIM>
+__device__ __forceinline__ double prolong_vertex_node(const double* __restrict__ zc, double* __restrict__ z, int3 nv,
+                                                      int3 N, int3 n, const Basis1D& bs, unsigned g) {
+  // 32-bit index arithmetic (grids below 2^31 nodes, checked by the caller)
   const unsigned gxy = g / (unsigned)N.x;
   const int gc[3] = {(int)(g - gxy * N.x), (int)(gxy % (unsigned)N.y), (int)(gxy / (unsigned)N.y)};
   const int Nn[3] = {N.x, N.y, N.z}, nn[3] = {n.x, n.y, n.z};
   bool dir = false;
 #pragma unroll
   for (int k = 0; k < DIM; ++k) if (gc[k] == 0 || gc[k] == Nn[k] - 1) dir = true;
-  if (dir) { z[g] = 0.0; return; }
+  if (dir) { z[g] = 0.0; return 0.0; }
   const int p = bs.p;
   int v0[3] = {0, 0, 0};
   double w0[3] = {1, 1, 1}, w1[3] = {0, 0, 0};
@@ -82,7 +107,9 @@ __global__ void k_prolong_vertex_add(const double* __restrict__ zc, double* __re
     }
     acc += w * __ldg(zc + vb + off);  // w = 0 terms read an existing vertex (clamped element)
   }
-  z[g] += acc;
+  const double zn = z[g] + acc;
+  z[g] = zn;
+  return zn;
 }
 
 // l1-Jacobi diagonal over interior columns of interior rows
@@ -156,28 +183,16 @@ __global__ void k_prolong_grid_add(const double* __restrict__ e, double* __restr
 }
 // coarsest GMG level: dense LDL^T over its interior nodes (one block)
 
-template <int DIM>
-__global__ void k_coarsest_solve(const double* __restrict__ F, const double* __restrict__ r, double* __restrict__ z,
-                                 int3 Nv, int nint) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const long long NT = (long long)Nv.x * Nv.y * Nv.z;
-  double x[64];
-  int idx = 0;
-  for (long long g = 0; g < NT; ++g) { int c[3]; if (interior_of<DIM>(g, Nv, c)) x[idx++] = r[g]; }
-  for (int i = 0; i < nint; ++i) {
-    double s = x[i];
-    for (int k = 0; k < i; ++k) s -= F[i * nint + k] * x[k];
-    x[i] = s / F[i * nint + i];
-  }
-  for (int i = nint - 1; i >= 0; --i) {
-    double s = x[i];
-    for (int k = i + 1; k < nint; ++k) s -= F[k * nint + i] * x[k];
-    x[i] = s / F[i * nint + i];
-  }
-  idx = 0;
-  for (long long g = 0; g < NT; ++g) { int c[3]; z[g] = interior_of<DIM>(g, Nv, c) ? x[idx++] : 0.0; }
+// z = C^{-1} r on the coarsest interior (dense symmetric inverse, thread = row; the
+// column walk makes the loads of a warp coalesced); boundary entries of z stay 0
+__global__ void k_coarsest_inv(const double* __restrict__ Cinv, const int* __restrict__ idx,
+                               const double* __restrict__ r, double* __restrict__ z, int nint) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nint) return;
+  double acc = 0.0;
+  for (int j = 0; j < nint; ++j) acc = fma(Cinv[(size_t)j * nint + i], __ldg(r + idx[j]), acc);
+  z[idx[i]] = acc;
 }
-
 
 // ------------------------------------------------------------------ patch V-cycle
 // VG = 8 lanes per patch, 4 patches per warp.  Shared memory per patch: the level
@@ -527,7 +542,8 @@ static int gmg_vcycle_t(const lorpc_prec* b, const double** out, cudaStream_t s)
     LORPC_LAUNCHED();
   }
   if (b->ncoarsest > 0) {
-    k_coarsest_solve<DIM><<<1, 1, 0, s>>>(b->coarse_chol, b->cr[K], b->cz[K], i3(b->cn[K]), b->ncoarsest);
+    k_coarsest_inv<<<nb(b->ncoarsest, 128), 128, 0, s>>>(b->coarse_chol, b->coarse_idx, b->cr[K], b->cz[K],
+                                                          b->ncoarsest);
     LORPC_LAUNCHED();
   } else {
     LORPC_CUDA(cudaMemsetAsync(b->cz[K], 0, sizeof(double) * b->cN[K], s));
@@ -549,8 +565,8 @@ int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStr
   int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, m->d == 3 ? m->n[2] + 1 : 1);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]), n = make_int3(m->n[0], m->n[1], m->n[2]);
   if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "prolong_vertex_add: grid of 2^31 nodes or more");
-  if (m->d == 2) k_prolong_vertex_add<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
-  else k_prolong_vertex_add<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis);
+  if (m->d == 2) k_prolong_vertex_add<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis, nullptr, nullptr);
+  else k_prolong_vertex_add<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(zc, z, nv, N, n, m->basis, nullptr, nullptr);
   LORPC_LAUNCHED();
   return LORPC_OK;
 }
@@ -558,18 +574,27 @@ int gmg_vcycle(const lorpc_prec* b, const double** out, cudaStream_t s) {
   return b->m->d == 2 ? gmg_vcycle_t<2>(b, out, s) : gmg_vcycle_t<3>(b, out, s);
 }
 
+// R_0 part of B (a7), split so that P_0^T r and the GMG V-cycle run on the aux stream
+// concurrently with the patch batch ("each of the local approximate solvers R_j
+// may be applied in parallel"); the prolongation P_0 z_0 joins on s.
 template <int DIM>
-static int coarse_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+static int coarse_restrict_solve(const lorpc_prec* b, const double* r, const double** z0, cudaStream_t s) {
+  const lorpc_mesh* m = b->m;
+  int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, DIM == 3 ? m->n[2] + 1 : 1);
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
+  k_restrict_vertex<DIM><<<nb(b->cN[0], 128), 128, 0, s>>>(r, b->cr[0], nv, N, m->basis);
+  LORPC_LAUNCHED();
+  return gmg_vcycle_t<DIM>(b, z0, s);
+}
+template <int DIM>
+static int coarse_prolong(const lorpc_prec* b, const double* z0, double* z, const double* rdot, double* part,
+                          cudaStream_t s) {
   const lorpc_mesh* m = b->m;
   int3 nv = make_int3(m->n[0] + 1, m->n[1] + 1, DIM == 3 ? m->n[2] + 1 : 1);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
-  k_restrict_vertex<DIM><<<nb(b->cN[0], 128), 128, 0, s>>>(r, b->cr[0], nv, N, m->basis);
-  LORPC_LAUNCHED();
-  const double* z0 = nullptr;
-  LORPC_TRY(gmg_vcycle_t<DIM>(b, &z0, s));
   if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "coarse_apply: grid of 2^31 nodes or more");
-  k_prolong_vertex_add<DIM><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z0, z, nv, N, n, m->basis);
+  k_prolong_vertex_add<DIM><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z0, z, nv, N, n, m->basis, rdot, part);
   LORPC_LAUNCHED();
   return LORPC_OK;
 }
@@ -640,9 +665,22 @@ int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaS
   return b->m->d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
 }
 
-int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart) {
   const lorpc_mesh* m = b->m;
   const int d = m->d;
+  const bool coarse = b->desc.coarse == 0;
+  const double* z0 = nullptr;
+  // R_0 concurrently with the patch batch on the aux stream is opt-in (LORPC_OVERLAP=1):
+  // measured on C5 it slows the thread-mode V-cycle from 42 to 60 ms per apply
+  // (DESIGN.md 5.2), far more than the ~1 ms the R_0 chain takes serially
+  static const int overlap = getenv("LORPC_OVERLAP") ? atoi(getenv("LORPC_OVERLAP")) : 0;
+  if (coarse && overlap) {  // fork: R_0 chain on the aux stream
+    LORPC_CUDA(cudaEventRecord(b->evf, s));
+    LORPC_CUDA(cudaStreamWaitEvent(b->aux, b->evf, 0));
+    if (d == 2) LORPC_TRY(coarse_restrict_solve<2>(b, r, &z0, b->aux));
+    else LORPC_TRY(coarse_restrict_solve<3>(b, r, &z0, b->aux));
+    LORPC_CUDA(cudaEventRecord(b->evj, b->aux));
+  }
   LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * m->ndof_cg, s));
   VcParams P = make_params(b, r, z);
   lorpc_prec* bm = const_cast<lorpc_prec*>(b);
@@ -654,9 +692,18 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   if (rc != LORPC_OK) return rc;
   if (prof) { LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n + 1], s)); bm->prof_n++; }
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
-  if (b->desc.coarse == 0) {
-    if (d == 2) LORPC_TRY(coarse_apply<2>(b, r, z, s)); else LORPC_TRY(coarse_apply<3>(b, r, z, s));
+  if (coarse) {  // join, then z += P_0 z_0 (and z_D = 0)
+    if (overlap) {
+      LORPC_CUDA(cudaStreamWaitEvent(s, b->evj, 0));
+    } else if (d == 2) {
+      LORPC_TRY(coarse_restrict_solve<2>(b, r, &z0, s));
+    } else {
+      LORPC_TRY(coarse_restrict_solve<3>(b, r, &z0, s));
+    }
+    if (d == 2) LORPC_TRY(coarse_prolong<2>(b, z0, z, rzpart ? r : nullptr, rzpart, s));
+    else LORPC_TRY(coarse_prolong<3>(b, z0, z, rzpart ? r : nullptr, rzpart, s));
   } else {
+    if (rzpart) return fail(LORPC_ERR_ARG, "schwarz_apply_cg: fused r.z needs the coarse term");
     if (d == 2) k_zero_dir<2><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z, N);
     else k_zero_dir<3><<<nb(m->ndof_cg, 256), 256, 0, s>>>(z, N);
     LORPC_LAUNCHED();

@@ -55,13 +55,14 @@ std::vector<int> tile_order(const lorpc_prec* b, int TX, int TY) {
 // factor is stored once and the backward sweep re-reads, in reverse, what the
 // forward sweep has just pulled through L2:
 //   int4 {S, Kp, 0, 0}: S steps (largest patch of the warp), Kp pair rows
-//   hdr[S][32]  u32  node k (bits 0-7) | count (bits 8-15) | mp (bits 16-23): pair
+//   hdr[S][32]  u32  node k (bits 0-15) | count (bits 16-23) | mp (bits 24-31): pair
 //                    rows of step t (the warp maximum, the same in every lane)
 //   Dinv[S][32] f64  1 / D_k
 //   Lc[Kp][32]  f64x2 column entries in pairs (one 16-byte load per lane and pair)
-//   Ic[Kp][32]  u8x2  their node indices i
+//   Ic[Kp][32]  their node indices i: u8x2 when the largest patch has <= 254 nodes
+//               (tiw = 1: C5, C2), else u16x2 (tiw = 2: C3)
 // Padding entries carry L = 0 and the dummy node n0max, padding steps the dummy
-// node with count 0 (node indices are u8: thread mode requires n0max <= 254).
+// node with count 0.
 struct TRecLayout { long long hdr, D, Lc, Ic, total; };
 // node index width of a warp's records: 1 byte when the largest patch has <= 254
 // nodes (C5, C2), else 2 bytes (C3)

@@ -43,7 +43,7 @@ class PcgReport(ctypes.Structure):
 SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc_quad_points",
            "lorpc_rhs_assemble", "lorpc_operator_apply", "lorpc_lor_assemble", "lorpc_lor_destroy",
            "lorpc_schwarz_setup", "lorpc_prec_destroy", "lorpc_precond_apply",
-           "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_prec_bytes", "lorpc_prec_profile",
+           "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_prec_kernel", "lorpc_prec_bytes", "lorpc_prec_profile",
            "lorpc_prec_profile_read", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
            "lorpc_launch_count", "lorpc_last_error",
            "lorpc_dist_plan_get", "lorpc_dist_nccl_id", "lorpc_dist_create", "lorpc_dist_destroy",
@@ -77,6 +77,7 @@ def lib():
         L.lorpc_precond_apply.argtypes = [_vp, _vp, _vp, _vp]
         L.lorpc_prec_export_ordering.argtypes = [_vp, _ll, _int, ctypes.POINTER(_int), ctypes.POINTER(_int)]
         L.lorpc_prec_info.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_int)]
+        L.lorpc_prec_kernel.argtypes = [_vp, ctypes.POINTER(_int)]
         L.lorpc_prec_bytes.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
         L.lorpc_prec_profile.argtypes = [_vp, _int]
         L.lorpc_prec_profile_read.argtypes = [_vp, ctypes.POINTER(_d), ctypes.POINTER(_ll)]
@@ -194,6 +195,16 @@ class Prec:
 
     def apply(self, r, z, stream=None):
         _check(lib().lorpc_precond_apply(self.h, _dptr(r), _dptr(z), _stream(stream)))
+
+    KERNELS = {0: "group-mode patch V-cycle (k_vcycle, every level in shared memory)",
+               1: "thread-mode patch V-cycle (k_vt_smooth pre + k_vt_mid + k_vt_smooth post)",
+               2: "W-mode fused patch V-cycle (k_vw, factor staged in shared memory)"}
+
+    def kernel(self):
+        """Label of the patch V-cycle kernel family this preconditioner runs."""
+        m = _int()
+        _check(lib().lorpc_prec_kernel(self.h, ctypes.byref(m)))
+        return self.KERNELS[m.value]
 
     def byte_model(self):
         """(factor values, [level-l grid nodes], coarse GMG nodes) for the roofline model."""
