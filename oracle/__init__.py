@@ -67,6 +67,10 @@ def lib():
         L.or_l2_error.argtypes = [_vp, _dp, _dp, _int]
         L.or_chain.argtypes = [_int, _ip, _ip]
         L.or_lor_assemble.argtypes = [_vp]
+        L.or_nsub.restype = _i64
+        L.or_nsub.argtypes = [_vp]
+        L.or_set_coefficient.argtypes = [_vp, _dp, _dp]
+        L.or_subcell_points.argtypes = [_vp, _dp]
         L.or_level_nnz.restype = _i64
         L.or_level_nnz.argtypes = [_vp, _int]
         L.or_level_n.restype = _i64
@@ -211,6 +215,22 @@ class Problem:
         X = np.zeros((nq, self.dim))
         lib().or_quad_points(self.h, _ptr(X))
         return X
+
+    def subcell_points(self):
+        """Gauss points of the LOR subcells, [n_sub * 2^d, d] (global subcell index
+        major, Gauss point bits x, y, z minor)."""
+        ns = lib().or_nsub(self.h) * (1 << self.dim)
+        X = np.zeros((ns, self.dim))
+        lib().or_subcell_points(self.h, _ptr(X))
+        return X
+
+    def set_coefficient(self, bq, bs):
+        """b(x) of -div(b grad u) at the volume Gauss points and the LOR subcell Gauss
+        points (row f3); None = 1."""
+        self._bq = None if bq is None else np.ascontiguousarray(bq, dtype=np.float64)
+        self._bs = None if bs is None else np.ascontiguousarray(bs, dtype=np.float64)
+        _check(lib().or_set_coefficient(self.h, None if self._bq is None else _ptr(self._bq),
+                                        None if self._bs is None else _ptr(self._bs)))
 
     def rhs(self, fq):
         fq = np.ascontiguousarray(fq, dtype=np.float64)

@@ -344,6 +344,12 @@ struct Mesh {
   i64 nel = 0, ndof = 0, nvert = 0;
   vec V;                  // [nvert][d]
   Basis b;
+  // variable coefficient b(x) of -div(b grad u) (sec:variable-coeff; row
+  // f3), sampled by the harness: bq[e][iq] at the volume Gauss points (or_quad_points
+  // layout), bs[sub][ig] at the 2^d Gauss points of every LOR subcell (global subcell
+  // index sx + (N0-1)(sy + (N1-1) sz), or_subcell_points layout).  Empty: b = 1.
+  vec bq, bs;
+  i64 sub_index(const int* sg) const { return sg[0] + (i64)(N[0] - 1) * (sg[1] + (i64)(N[1] - 1) * sg[2]); }
 
   void elem_coords(i64 e, int* ec) const {
     ec[0] = (int)(e % n[0]); i64 r = e / n[0];
@@ -429,6 +435,7 @@ static bool elem_stiffness(const Mesh& m, i64 e, vec& K) {
       }
     }
     double f = w * det;
+    if (!m.bq.empty()) f *= m.bq[(size_t)e * nq + iq];   // b(x_q) (sec:variable-coeff)
     for (int a = 0; a < nl; ++a)
       for (int bb = 0; bb < nl; ++bb) {
         double s = 0.0;
@@ -513,6 +520,62 @@ extern "C" int or_set_dg(void* h, int disc, double eta) {
 }
 
 extern "C" i64 or_ndof(void* h) { return ((Problem*)h)->m.ndof; }
+
+// Variable coefficient (row f3): bq [nquad] at the volume Gauss points, bs [nsub][2^d]
+// at the LOR subcell Gauss points (either may be NULL = 1).  CG only.  Invalidates the
+// cached element matrices, the LOR hierarchy and the Schwarz setup.
+extern "C" i64 or_nsub(void* h) {
+  const Mesh& m = ((Problem*)h)->m;
+  i64 n = 1;
+  for (int k = 0; k < m.d; ++k) n *= m.N[k] - 1;
+  return n;
+}
+extern "C" int or_set_coefficient(void* h, const double* bq, const double* bs) {
+  Problem* P = (Problem*)h;
+  Mesh& m = P->m;
+  if (P->disc != 0) { g_err = "coefficient: CG only"; return 1; }
+  const int q = m.b.q, nq = m.d == 2 ? q * q : q * q * q;
+  if (bq) m.bq.assign(bq, bq + m.nel * nq); else m.bq.clear();
+  if (bs) m.bs.assign(bs, bs + or_nsub(h) * (1 << m.d)); else m.bs.clear();
+  for (double v : m.bq) if (!(v > 0.0)) { g_err = "coefficient: b <= 0"; return 1; }
+  for (double v : m.bs) if (!(v > 0.0)) { g_err = "coefficient: b <= 0"; return 1; }
+  P->Kel.clear(); P->cached = false;
+  P->lor_built = false; P->schwarz_built = false;
+  return 0;
+}
+// Gauss points of every LOR subcell: X[sub][ig][d], the subcell map multilinear in
+// the images of its corner GLL nodes (reading c2), t = 1/2 -+ 1/(2 sqrt 3).
+extern "C" void or_subcell_points(void* h, double* X) {
+  const Mesh& m = ((Problem*)h)->m;
+  const int d = m.d, p = m.p, nc = 1 << d;
+  const double gp[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  const int nsub = d == 2 ? p * p : p * p * p;
+  for (i64 e = 0; e < m.nel; ++e)
+    for (int s = 0; s < nsub; ++s) {
+      int sc[3] = {s % p, (s / p) % p, (d == 3) ? s / (p * p) : 0}, ec[3], sg[3] = {0, 0, 0};
+      m.elem_coords(e, ec);
+      for (int k = 0; k < d; ++k) sg[k] = ec[k] * p + sc[k];
+      double Xc[8][3];
+      for (int c = 0; c < nc; ++c) {
+        double xi[3], x[3], J[9];
+        for (int k = 0; k < d; ++k) xi[k] = m.b.xi[sc[k] + ((c >> k) & 1)];
+        m.map(e, xi, x, J);
+        for (int k = 0; k < d; ++k) Xc[c][k] = x[k];
+      }
+      for (int ig = 0; ig < nc; ++ig) {
+        double* o = X + ((size_t)m.sub_index(sg) * nc + ig) * d;
+        for (int i = 0; i < d; ++i) o[i] = 0.0;
+        for (int c = 0; c < nc; ++c) {
+          double wv = 1.0;
+          for (int k = 0; k < d; ++k) {
+            const double t = gp[(ig >> k) & 1];
+            wv *= ((c >> k) & 1) ? t : 1.0 - t;
+          }
+          for (int i = 0; i < d; ++i) o[i] += wv * Xc[c][i];
+        }
+      }
+    }
+}
 
 // Element stiffness matrix for tests.
 extern "C" int or_elem_matrix(void* h, i64 e, double* out) {
@@ -732,6 +795,12 @@ static bool assemble_Kh(const Mesh& m, CSR& K) {
         double det = det_inv(d, J, Ji);
         if (!(det > 0.0)) ok = false;
         double w = (d == 2) ? 0.25 : 0.125;
+        if (!m.bs.empty()) {   // b sampled at the subcell Gauss point (SPEC S:233 reading)
+          int ec[3], sg[3] = {0, 0, 0};
+          m.elem_coords(e, ec);
+          for (int k = 0; k < d; ++k) sg[k] = ec[k] * p + sc[k];
+          w *= m.bs[(size_t)m.sub_index(sg) * nc + ig];
+        }
         double pg[8][3];
         for (int c = 0; c < nc; ++c)
           for (int i = 0; i < d; ++i) {

@@ -180,3 +180,40 @@ def br2_1d(p, n, eta):
             pen = eta * Minv[p, p]
         A += -np.outer(jm, av) - np.outer(av, jm) + pen * np.outer(jm, jm)
     return A, M
+
+
+# ---------------------------------------------------------------- weighted 1D matrices (row f3 pins)
+def fe_1d_weighted(p, n, bfun, length=1.0, extra=3):
+    """1D high-order stiffness and mass with weight b(x), integrated with a Gauss rule
+    of p+1+extra points per element (exact for polynomial b of degree <= 2 extra)."""
+    xi = gll_nodes(p)
+    tg, wg = gauss(p + 1 + extra)
+    B, D = lagrange_tables(xi, tg)
+    h = length / n
+    N = n * p + 1
+    K = np.zeros((N, N))
+    M = np.zeros((N, N))
+    for e in range(n):
+        bw = wg * bfun(e * h + h * tg)
+        s = slice(e * p, e * p + p + 1)
+        K[s, s] += D.T @ np.diag(bw) @ D / h
+        M[s, s] += B.T @ np.diag(bw) @ B * h
+    return K, M
+
+
+def p1_1d_weighted(points, bfun):
+    """Piecewise-linear stiffness / mass with weight b(x) on a 1D grid (4-point Gauss
+    per interval: exact for b of degree <= 5)."""
+    tg, wg = gauss(4)
+    N = len(points)
+    K = np.zeros((N, N))
+    M = np.zeros((N, N))
+    for i in range(N - 1):
+        a, h = points[i], points[i + 1] - points[i]
+        x = a + h * tg
+        bw = wg * bfun(x)
+        phi = np.stack([1 - tg, tg])
+        dphi = np.array([-1.0, 1.0]) / h
+        K[i:i + 2, i:i + 2] += np.outer(dphi, dphi) * bw.sum() * h
+        M[i:i + 2, i:i + 2] += (phi * bw) @ phi.T * h
+    return K, M

@@ -106,3 +106,53 @@ def parity_vector(n: int, seed: int = 42) -> np.ndarray:
 def small_config(name: str, n, p=None) -> Config:
     from .configs import CONFIGS
     return shrink(CONFIGS[name], tuple(n), p)
+
+
+# ------------------------------------------------------------------ variable coefficients (row f3)
+COEFF_SEED = 9011
+
+
+def coefficient_function(kind: str, X: np.ndarray) -> np.ndarray:
+    """b(x, y) of -div(b grad u) (sec:variable-coeff).  The paper's
+    domain is [-1,1]^2; ours is [0,1]^d, mapped by x' = 2x - 1 (reading r4).
+      b1 = 1e4 (1 - x'^2)(1 - y'^2), b2 = 100 x'^2 + y'^2 + 1, b3 = (1 + x'^2 + y'^2)^4."""
+    xp = 2.0 * X[:, 0] - 1.0
+    yp = 2.0 * X[:, 1] - 1.0
+    if kind == "b1":
+        return 1e4 * (1.0 - xp * xp) * (1.0 - yp * yp)
+    if kind == "b2":
+        return 100.0 * xp * xp + yp * yp + 1.0
+    if kind == "b3":
+        return (1.0 + xp * xp + yp * yp) ** 4
+    if kind == "one":
+        return np.ones(X.shape[0])
+    raise ValueError(kind)
+
+
+def coefficient_b4(n_el: int, seed: int = COEFF_SEED) -> np.ndarray:
+    """b4: piecewise constant, 10 or 1 per element, drawn at random (P:894-895);
+    i.i.d. fair draws with PCG64(seed), elements in x-fastest order."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.where(rng.random(n_el) < 0.5, 10.0, 1.0)
+
+
+def coefficient_samples(kind: str, cfg: Config, Xq: np.ndarray, Xs: np.ndarray):
+    """(b at the volume quadrature points, b at the LOR subcell Gauss points) for
+    coefficient `kind`.  Xq is [n_el * q^d, d] element-major (the layout of
+    quad_points), Xs is [n_sub * 2^d, d] with the global subcell index
+    sx + (N0-1)(sy + (N1-1) sz) major (the layout of subcell_points).  b4 needs no
+    coordinates: each point takes its element's value."""
+    if kind != "b4":
+        return coefficient_function(kind, Xq), coefficient_function(kind, Xs)
+    be = coefficient_b4(cfg.n_el)
+    nq = Xq.shape[0] // cfg.n_el
+    bq = np.repeat(be, nq)
+    d, p = cfg.dim, cfg.p
+    Ns = [n * p for n in cfg.n]                       # subcells per axis
+    ns = int(np.prod(Ns))
+    s = np.arange(ns)
+    sc = [s % Ns[0], (s // Ns[0]) % Ns[1]] + ([s // (Ns[0] * Ns[1])] if d == 3 else [])
+    ec = [c // p for c in sc]
+    e = ec[0] + cfg.n[0] * (ec[1] + (cfg.n[1] * ec[2] if d == 3 else 0))
+    bs = np.repeat(be[e], 1 << d)
+    return bq, bs
