@@ -62,12 +62,16 @@ typedef struct {
                    LORPC_ERR_SIZE otherwise).  DG requires dim = 3. */
   double eta;   /* SIPG: sigma_e = eta / h_e, h_e = min(|K-|,|K+|)/|e| (readings c13, c14);
                    BR2: coefficient of sum_e (r_e([u]), r_e([v])) */
+  int quad;     /* volume quadrature: 0 = Gauss q = p+1 (reading c1), 1 = GLL collocation
+                   (the p+1 GLL nodes per direction; SURVEY row f2, P:785-793 quadrature
+                   variant).  quad = 1 requires disc = 0 (LORPC_ERR_ARG otherwise). */
 } lorpc_mesh_desc;
 
 /* Additive Schwarz B = sum_{j=0}^J R_j Q_j (eq:as P:274-277). */
 typedef struct {
   int patch_kind; /* 0 = vertex patches (eq:patch P:302-315), 1 = element star (reading c9) */
-  int ordering;   /* ILU(0) ordering: 0 = minimum discarded fill, 1 = natural */
+  int ordering;   /* ILU(0) ordering: 0 = minimum discarded fill, 1 = natural,
+                     2 = reverse Cuthill-McKee (structure only, reading r5) */
   int coarse;     /* 0 = R_0 one GMG V(1,1) with l1-Jacobi (reading c11), 1 = no coarse term */
 } lorpc_schwarz_desc;
 
@@ -97,6 +101,21 @@ int lorpc_mesh_sizes(const lorpc_mesh* m, long long* n_dof, long long* n_quad, l
  * axis, side low/high, elements ascending, face points lower axis fastest);
  * either output may be NULL. */
 int lorpc_quad_points(const lorpc_mesh* m, double* xq_dev, double* xbq_dev, void* stream);
+/* Variable coefficient b(x) of -div(b grad u) (row f3; P:881-901,
+ * sec:variable-coeff, coefficients b1..b4 there).  bq_dev [n_quad] = b at the
+ * volume Gauss points in the lorpc_quad_points order (enters K_p as b(x_q) w_q
+ * det J J^{-1} J^{-T}); bsub_dev [n_sub * 2^d] = b at the Gauss points of the LOR
+ * subcells in the lorpc_subcell_points order (enters K_h, sampled pointwise: SPEC
+ * S:233 reading).  Either may be NULL (b = 1).  Device arrays, copied; the mesh's
+ * geometric factors are re-formed.  Must precede lorpc_lor_assemble.  CG meshes
+ * only.  Errors: LORPC_ERR_ARG (DG mesh, a value <= 0). */
+int lorpc_mesh_set_coefficient(lorpc_mesh* m, const double* bq_dev, const double* bsub_dev, void* stream);
+/* Gauss points of the LOR subcells (2^d per subcell, t = 1/2 -+ 1/(2 sqrt 3) on the
+ * subcell map multilinear in its corner GLL node images, reading c2): xs_dev
+ * [n_sub][2^d][d], subcell index sx + (N0-1)(sy + (N1-1) sz) major (N = GLL nodes per
+ * axis), Gauss-point bits x, y, z minor; *n_sub = number of subcells.  xs_dev may be
+ * NULL (size query only). */
+int lorpc_subcell_points(const lorpc_mesh* m, double* xs_dev, long long* n_sub, void* stream);
 /* Load vector b = (f, v) (eq:fem) from f at the volume Gauss points; CG:
  * Dirichlet rows zeroed; DG: plus the symmetric Nitsche boundary data
  * int_e (sigma_e g v - g d_n v) from g at the boundary points (gq_dev may be

@@ -54,6 +54,7 @@ def lib():
         L.or_create.argtypes = [_int, _int, _int, _int, _int, _dp]
         L.or_destroy.argtypes = [_vp]
         L.or_set_dg.argtypes = [_vp, _int, _d]
+        L.or_set_quad.argtypes = [_vp, _int]
         L.or_ndof.restype = _i64
         L.or_ndof.argtypes = [_vp]
         L.or_elem_matrix.argtypes = [_vp, _i64, _dp]
@@ -153,14 +154,14 @@ def mdf_ilu(A, ordering=0, r=None):
 
 
 PATCH_KIND = {"vertex": 0, "star": 1, "single": 2}
-ORDERING = {"mdf": 0, "natural": 1}
+ORDERING = {"mdf": 0, "natural": 1, "rcm": 2}
 COARSE = {"gmg": 0, "none": 1, "exact": 2}
 
 
 class Problem:
     """One discretised problem: mesh, operator, LOR, Schwarz, PCG (all CPU)."""
 
-    def __init__(self, dim, n, p, V, disc="cg", eta=0.0):
+    def __init__(self, dim, n, p, V, disc="cg", eta=0.0, quad="gauss"):
         n = list(n) + [1] * (3 - len(n))
         self.dim, self.n, self.p = dim, n[:dim], p
         V = np.ascontiguousarray(V, dtype=np.float64)
@@ -173,6 +174,8 @@ class Problem:
         self.n_el = int(np.prod(self.n))
         if disc != "cg":
             _check(lib().or_set_dg(self.h, {"sipg": 1, "br2": 2}[disc], float(eta)))
+        if quad != "gauss":
+            _check(lib().or_set_quad(self.h, {"gll": 1}[quad]))
         self.ndof_cg = lib().or_ndof(self.h)
         self.ndof = self.ndof_cg if disc == "cg" else self.n_el * self.nloc
 

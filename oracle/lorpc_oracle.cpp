@@ -149,12 +149,14 @@ static double dlagrange(const vec& xn, int j, double t) {
 struct Basis {
   int p, q;
   vec xi, wgll;  // GLL nodes / weights on [0,1]
-  vec xg, wg;    // Gauss nodes / weights on [0,1], q = p+1 (reading c1)
+  vec xg, wg;    // volume rule on [0,1], q = p+1 points: Gauss (reading c1) or, with
+                 // quad = 1, the GLL nodes themselves (collocation)
   vec B, D;      // [q][p+1]: l_j(xg_i), l_j'(xg_i)
-  void init(int p_) {
+  void init(int p_, int quad = 0) {
     p = p_; q = p + 1;
     gll_rule(p, xi, wgll);
-    gauss_rule(q, xg, wg);
+    if (quad == 1) { xg = xi; wg = wgll; }
+    else gauss_rule(q, xg, wg);
     B.assign(q * (p + 1), 0.0); D.assign(q * (p + 1), 0.0);
     for (int i = 0; i < q; ++i)
       for (int j = 0; j <= p; ++j) {
@@ -467,7 +469,7 @@ struct Problem {
   int disc = 0;           // 0 = CG, 1 = SIPG
   double eta = 0.0;       // SIPG penalty coefficient: sigma_e = eta / h_e (reading c13)
   int patch_kind = 0;     // 0 = vertex (eq:patch), 1 = element star (reading c9)
-  int ordering = 0;       // 0 = MDF, 1 = natural
+  int ordering = 0;       // 0 = MDF, 1 = natural, 2 = RCM (reading r5)
   int coarse = 0;         // 0 = GMG l1-Jacobi R_0 (reading c11), 1 = none, 2 = exact (dense)
   int local_exact = 0;    // 1: R_j = A_j^{-1} (dense Cholesky) instead of the V-cycle (pins only)
   std::vector<vec> Kel;   // cached element matrices (CG) or empty
@@ -512,6 +514,17 @@ extern "C" void* or_create(int d, int n0, int n1, int n2, int p, const double* v
   return P;
 }
 extern "C" void or_destroy(void* h) { delete (Problem*)h; }
+
+// Volume quadrature: 0 = Gauss q = p+1 (reading c1), 1 = GLL collocation (the
+// quadrature points are the nodes; row f2's quadrature variant).  CG only.
+extern "C" int or_set_quad(void* h, int quad) {
+  Problem* P = (Problem*)h;
+  if (quad != 0 && quad != 1) { g_err = "quad must be 0 or 1"; return 1; }
+  if (quad == 1 && P->disc != 0) { g_err = "GLL collocation: CG only"; return 1; }
+  P->m.b.init(P->m.p, quad);
+  P->Kel.clear(); P->cached = false;
+  return 0;
+}
 
 extern "C" int or_set_dg(void* h, int disc, double eta) {
   Problem* P = (Problem*)h;
@@ -971,6 +984,38 @@ static double mdf_weight2(const CSR& A, const vec& At, const std::vector<char>& 
   return s;
 }
 
+// Reverse Cuthill-McKee on the sparsity graph of A (P:599 cites it; definition and
+// ties are reading r5): start at a node of minimum degree (lowest index
+// among ties), breadth-first, each node's unvisited neighbours appended in order of
+// (degree, index), restart at the next minimum-degree node if the graph is not
+// connected; the elimination order is the reverse of the visiting order.
+static std::vector<int> rcm_order(const CSR& A) {
+  const int n = (int)A.nr;
+  std::vector<int> deg(n, 0), seq, nb;
+  std::vector<char> seen(n, 0);
+  for (int i = 0; i < n; ++i)
+    for (i64 a = A.rp[i]; a < A.rp[i + 1]; ++a) if (A.ci[a] != i) ++deg[i];
+  while ((int)seq.size() < n) {
+    int s = -1;
+    for (int i = 0; i < n; ++i) if (!seen[i] && (s < 0 || deg[i] < deg[s])) s = i;
+    seen[s] = 1;
+    size_t head = seq.size();
+    seq.push_back(s);
+    while (head < seq.size()) {
+      const int v = seq[head++];
+      nb.clear();
+      for (i64 a = A.rp[v]; a < A.rp[v + 1]; ++a) {
+        const int u = A.ci[a];
+        if (u != v && !seen[u]) { seen[u] = 1; nb.push_back(u); }
+      }
+      std::sort(nb.begin(), nb.end(), [&](int x, int y) { return deg[x] < deg[y] || (deg[x] == deg[y] && x < y); });
+      seq.insert(seq.end(), nb.begin(), nb.end());
+    }
+  }
+  std::reverse(seq.begin(), seq.end());
+  return seq;
+}
+
 static bool mdf_ilu(PatchLevel& L, int ordering) {
   const CSR& A = L.A; int n = L.n;
   vec At = A.v;
@@ -980,13 +1025,16 @@ static bool mdf_ilu(PatchLevel& L, int ordering) {
   L.Lv.assign(A.nnz(), 0.0); L.Dg.assign(n, 0.0);
   if (ordering == 0)
     for (int k = 0; k < n; ++k) w2[k] = mdf_weight2(A, At, alive, k);
+  const std::vector<int> rcm = ordering == 2 ? rcm_order(A) : std::vector<int>();
   for (int step = 0; step < n; ++step) {
     int kbest = -1; double key = 0.0;
-    for (int k = 0; k < n; ++k) {
-      if (!alive[k]) continue;
-      double kq = (ordering == 0) ? q30(w2[k]) : 0.0;
-      if (kbest < 0 || kq < key) { kbest = k; key = kq; }
-    }
+    if (ordering == 2) kbest = rcm[step];
+    else
+      for (int k = 0; k < n; ++k) {
+        if (!alive[k]) continue;
+        double kq = (ordering == 0) ? q30(w2[k]) : 0.0;
+        if (kbest < 0 || kq < key) { kbest = k; key = kq; }
+      }
     int k = kbest;
     L.order[step] = k; L.pos[k] = step;
     int kk = find_in_row(A, k, k);

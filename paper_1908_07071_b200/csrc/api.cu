@@ -46,6 +46,8 @@ int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, 
   for (int k = 0; k < d; ++k) if (desc->n[k] < 1) return fail(LORPC_ERR_ARG, "mesh_create: n must be >= 1");
   if (desc->disc < 0 || desc->disc > 2) return fail(LORPC_ERR_ARG, "mesh_create: disc must be 0 (CG), 1 (SIPG), 2 (BR2)");
   if (desc->disc != 0 && !(desc->eta > 0.0)) return fail(LORPC_ERR_ARG, "mesh_create: eta must be > 0");
+  if (desc->quad != 0 && desc->quad != 1) return fail(LORPC_ERR_ARG, "mesh_create: quad must be 0 (Gauss) or 1 (GLL)");
+  if (desc->quad == 1 && desc->disc != 0) return fail(LORPC_ERR_ARG, "mesh_create: GLL collocation is CG only");
   if (desc->disc != 0 && d != 3) return fail(LORPC_ERR_SIZE, "mesh_create: DG is built for 3D meshes");
   if (desc->disc == 2) {
     // the BR2 lifting kernels use M_K = det J (M1 x M1 x M1): elements must be affine
@@ -91,7 +93,7 @@ int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, 
     for (int k = 0; k < d; ++k) faces += 2 * (m->nel / m->n[k]);
     m->nbq = faces * (d == 2 ? m->q : m->q * m->q);
   }
-  make_basis(m->p, m->basis);
+  make_basis(m->p, m->basis, desc->quad);
   cudaStream_t s = S(stream);
   int rc = dalloc(&m->V, (size_t)nvert * d);
   if (rc == LORPC_OK) {
@@ -108,6 +110,7 @@ int lorpc_mesh_create(const lorpc_mesh_desc* desc, const double* vertices_host, 
 void lorpc_mesh_destroy(lorpc_mesh* m) {
   if (!m) return;
   dfree(m->V); dfree(m->G); dfree(m->X); dfree(m->vol); dfree(m->dgdiag); dfree(m->ywork);
+  dfree(m->bq); dfree(m->bsub);
   delete m;
 }
 
@@ -123,6 +126,19 @@ int lorpc_quad_points(const lorpc_mesh* m, double* xq_dev, double* xbq_dev, void
   if (!m) return fail(LORPC_ERR_ARG, "quad_points: NULL mesh");
   if (xbq_dev && m->desc.disc == 0) return fail(LORPC_ERR_ARG, "quad_points: boundary points only for DG");
   return quad_points(m, xq_dev, xbq_dev, S(stream));
+}
+
+int lorpc_mesh_set_coefficient(lorpc_mesh* m, const double* bq_dev, const double* bsub_dev, void* stream) {
+  if (!m) return fail(LORPC_ERR_ARG, "mesh_set_coefficient: NULL mesh");
+  if (m->desc.disc != 0) return fail(LORPC_ERR_ARG, "mesh_set_coefficient: CG meshes only");
+  return set_coefficient(m, bq_dev, bsub_dev, S(stream));
+}
+
+int lorpc_subcell_points(const lorpc_mesh* m, double* xs_dev, long long* n_sub, void* stream) {
+  if (!m) return fail(LORPC_ERR_ARG, "subcell_points: NULL mesh");
+  if (n_sub) *n_sub = n_subcells(m);
+  if (!xs_dev) return LORPC_OK;
+  return subcell_points(m, xs_dev, S(stream));
 }
 
 int lorpc_rhs_assemble(const lorpc_mesh* m, const double* fq_dev, const double* gq_dev, double* b_dev, void* stream) {
@@ -155,7 +171,7 @@ void lorpc_lor_destroy(lorpc_lor* l) {
 int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void* stream, lorpc_prec** out) {
   if (!l || !desc || !out) return fail(LORPC_ERR_ARG, "schwarz_setup: NULL argument");
   if (desc->patch_kind < 0 || desc->patch_kind > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: patch_kind");
-  if (desc->ordering < 0 || desc->ordering > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: ordering");
+  if (desc->ordering < 0 || desc->ordering > 2) return fail(LORPC_ERR_ARG, "schwarz_setup: ordering");
   if (desc->coarse < 0 || desc->coarse > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: coarse");
   *out = nullptr;
   lorpc_prec* b = new lorpc_prec();

@@ -26,7 +26,7 @@ static void leg(int n, long double x, long double& P, long double& dP) {
   dP = (std::fabs((double)x) < 1.0) ? n * (a - x * b) / (1.0L - x * x) : 0.5L * n * (n + 1) * (x > 0 ? 1.0L : ((n % 2) ? 1.0L : -1.0L));
 }
 
-void make_basis(int p, Basis1D& B) {
+void make_basis(int p, Basis1D& B, int quad) {
   B.p = p; B.q = p + 1;
   // GLL on [-1,1]: +-1 and the zeros of P_p'; Newton on P_p' with
   // (P_p')' = (2x P_p' - p(p+1) P_p) / (1 - x^2)
@@ -81,10 +81,22 @@ void make_basis(int p, Basis1D& B) {
       val[j] = v; der[j] = d;
     }
   };
+  if (quad == 1) {
+    // GLL collocation: the rule's points are the nodes, w_i = 2 / (p (p+1) P_p(t_i)^2)
+    // on [-1,1], halved on [0,1]
+    for (int i = 0; i <= p; ++i) {
+      long double P, dP;
+      leg(p, t[i], P, dP);
+      B.xq[i] = B.xi[i];
+      B.wq[i] = (double)(1.0L / ((long double)p * (p + 1) * P * P));
+    }
+  }
   long double v[MAXP + 1], d[MAXP + 1];
   for (int i = 0; i < q; ++i) {
     eval(B.xq[i], v, d);
     for (int j = 0; j <= p; ++j) { B.B[i * (p + 1) + j] = (double)v[j]; B.D[i * (p + 1) + j] = (double)d[j]; }
+    if (quad == 1)  // l_j(x_i) = delta_ij exactly
+      for (int j = 0; j <= p; ++j) B.B[i * (p + 1) + j] = i == j ? 1.0 : 0.0;
   }
   eval(0.0L, v, d); for (int j = 0; j <= p; ++j) B.E0[j] = (double)d[j];
   eval(1.0L, v, d); for (int j = 0; j <= p; ++j) B.E1[j] = (double)d[j];

@@ -51,14 +51,14 @@ void dfree(T*& p) { if (p) cudaFree((void*)p); p = nullptr; }
 struct Basis1D {
   int p, q;
   double xi[MAXP + 1];              // GLL nodes on [0,1]
-  double wq[MAXP + 1];              // Gauss weights on [0,1] (q = p+1, reading c1)
-  double xq[MAXP + 1];              // Gauss nodes
+  double wq[MAXP + 1];              // volume rule weights on [0,1] (q = p+1): Gauss (reading c1) or GLL
+  double xq[MAXP + 1];              // its nodes (GLL collocation: xq = xi)
   double B[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j(x_q)
   double D[(MAXP + 1) * (MAXP + 1)];  // [q][p+1]  l_j'(x_q)
   double E0[MAXP + 1], E1[MAXP + 1];  // l_j'(0), l_j'(1) (face normal derivatives)
   double M1inv[(MAXP + 1) * (MAXP + 1)];  // inverse of the reference 1D mass B^T W B (BR2 lifting)
 };
-void make_basis(int p, Basis1D& b);                 // basis.cpp
+void make_basis(int p, Basis1D& b, int quad = 0);   // basis.cpp (quad 1: GLL collocation)
 std::vector<std::vector<int>> make_chain(int p);    // basis.cpp (reading c3)
 
 // Per-element-local 1D prolongation table between hierarchy levels l+1 -> l:
@@ -87,6 +87,8 @@ struct lorpc_mesh {
   double* X = nullptr;              // [ndof_cg][d] node coordinates
   double* vol = nullptr;            // [nel] element volumes (DG)
   double* dgdiag = nullptr;         // [ndof] diag(A_IP) (DG)
+  double* bq = nullptr;             // [nel][nq] coefficient b at the volume Gauss points (row f3; NULL: 1)
+  double* bsub = nullptr;           // [nsub][2^d] b at the LOR subcell Gauss points (NULL: 1)
   double* ywork = nullptr;          // DG face workspace
 };
 
@@ -189,6 +191,9 @@ int prolong_vertex_add(const lorpc_mesh* m, const double* zc, double* z, cudaStr
 int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart = nullptr);
 long long rz_parts(const lorpc_prec* b);  // blocks of the fused r.z partial sums (0: not fused)
 int quad_points(const lorpc_mesh* m, double* xq, double* xbq, cudaStream_t s);
+int subcell_points(const lorpc_mesh* m, double* xs, cudaStream_t s);
+long long n_subcells(const lorpc_mesh* m);
+int set_coefficient(lorpc_mesh* m, const double* bq, const double* bs, cudaStream_t s);
 int rhs_assemble(const lorpc_mesh* m, const double* fq, const double* gq, double* b, cudaStream_t s);
 int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double* x, double rtol,
             int maxit, lorpc_pcg_report* rep, cudaStream_t s);

@@ -16,7 +16,8 @@
 namespace lorpc {
 
 template <int DIM>
-__global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __restrict__ A) {
+__global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __restrict__ A,
+                              const double* __restrict__ bsub) {
   constexpr int ND = Dirs<DIM>::ND, NC = 1 << DIM;
   const long long Ntot = (long long)N.x * N.y * N.z;
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -46,6 +47,8 @@ __global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __re
     double Kr[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) Kr[c] = 0.0;
+    // b at this subcell's Gauss points (row f3; global subcell index)
+    const long long sidx = sc[0] + (long long)(N.x - 1) * (sc[1] + (long long)(N.y - 1) * (DIM == 3 ? sc[2] : 0));
 #pragma unroll
     for (int ig = 0; ig < NC; ++ig) {
       const int gb[3] = {ig & 1, (ig >> 1) & 1, (ig >> 2) & 1};
@@ -87,7 +90,7 @@ __global__ void k_assemble_kh(const double* __restrict__ X, int3 N, double* __re
           for (int k = 0; k < DIM; ++k) v += Ji[k * DIM + i] * gr[c][k];
           s += pm[i] * v;
         }
-        Kr[c] += wgt * det * s;
+        Kr[c] += (bsub ? wgt * bsub[sidx * NC + ig] : wgt) * det * s;
       }
     }
 #pragma unroll
@@ -267,8 +270,8 @@ int lor_build(const lorpc_mesh* m, lorpc_lor* l, cudaStream_t s) {
   }
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   const unsigned g = (unsigned)((m->ndof_cg + 127) / 128);
-  if (d == 2) k_assemble_kh<2><<<g, 128, 0, s>>>(m->X, N, l->A[0]);
-  else k_assemble_kh<3><<<g, 128, 0, s>>>(m->X, N, l->A[0]);
+  if (d == 2) k_assemble_kh<2><<<g, 128, 0, s>>>(m->X, N, l->A[0], m->bsub);
+  else k_assemble_kh<3><<<g, 128, 0, s>>>(m->X, N, l->A[0], m->bsub);
   LORPC_LAUNCHED();
   for (int lv = 0; lv + 1 < l->L; ++lv)
     LORPC_TRY(galerkin(d, l->A[lv], l->A[lv + 1], l->T[lv], m->n, l->Nax[lv], l->Nax[lv + 1], s));

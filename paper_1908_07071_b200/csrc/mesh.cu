@@ -11,7 +11,7 @@ namespace lorpc {
 
 template <int DIM>
 __global__ void k_geom(const double* __restrict__ V, int3 n, Basis1D bs, double* __restrict__ G,
-                       double* __restrict__ vol, unsigned long long* bad) {
+                       double* __restrict__ vol, unsigned long long* bad, const double* __restrict__ bq) {
   const int q = bs.q;
   const int nq = DIM == 2 ? q * q : q * q * q;
   const long long nel = (long long)n.x * n.y * (DIM == 3 ? n.z : 1);
@@ -29,7 +29,8 @@ __global__ void k_geom(const double* __restrict__ V, int3 n, Basis1D bs, double*
   elem_map<DIM>(V, nv, ex, ey, ez, xi, x, J);
   const double det = inv_det<DIM>(J, Ji);
   if (!(det > 0.0)) atomicMin(bad, (unsigned long long)e);
-  const double f = w * det;
+  // b(x_q) w_q det J_q J^{-1} J^{-T} (sec:variable-coeff; b = 1 unless set)
+  const double f = w * det * (bq ? bq[tid] : 1.0);
   constexpr int NC = DIM == 2 ? 3 : 6;
   double* Ge = G + e * NC * nq;
   int c = 0;
@@ -43,7 +44,7 @@ __global__ void k_geom(const double* __restrict__ V, int3 n, Basis1D bs, double*
       Ge[c * nq + iq] = f * s;
       ++c;
     }
-  if (vol) atomicAdd(vol + e, f);
+  if (vol) atomicAdd(vol + e, w * det);
 }
 
 // Physical coordinates of the GLL nodes (images of the GLL grid under the
@@ -141,9 +142,9 @@ static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) 
 int geom_setup(lorpc_mesh* m, cudaStream_t s) {
   const int d = m->d;
   const int nc = d == 2 ? 3 : 6;
-  LORPC_TRY(dalloc(&m->G, (size_t)m->nel * nc * m->nq));
-  LORPC_TRY(dalloc(&m->X, (size_t)m->ndof_cg * d));
-  LORPC_TRY(dalloc(&m->vol, (size_t)m->nel));
+  if (!m->G) LORPC_TRY(dalloc(&m->G, (size_t)m->nel * nc * m->nq));
+  if (!m->X) LORPC_TRY(dalloc(&m->X, (size_t)m->ndof_cg * d));
+  if (!m->vol) LORPC_TRY(dalloc(&m->vol, (size_t)m->nel));
   LORPC_CUDA(cudaMemsetAsync(m->vol, 0, sizeof(double) * m->nel, s));
   unsigned long long* bad;
   LORPC_CUDA(cudaMallocHost(&bad, sizeof(unsigned long long)));
@@ -154,8 +155,8 @@ int geom_setup(lorpc_mesh* m, cudaStream_t s) {
   int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   long long tot = m->nel * m->nq;
-  if (d == 2) k_geom<2><<<nblk(tot, 128), 128, 0, s>>>(m->V, n, m->basis, m->G, m->vol, dbad);
-  else k_geom<3><<<nblk(tot, 128), 128, 0, s>>>(m->V, n, m->basis, m->G, m->vol, dbad);
+  if (d == 2) k_geom<2><<<nblk(tot, 128), 128, 0, s>>>(m->V, n, m->basis, m->G, m->vol, dbad, m->bq);
+  else k_geom<3><<<nblk(tot, 128), 128, 0, s>>>(m->V, n, m->basis, m->G, m->vol, dbad, m->bq);
   LORPC_LAUNCHED();
   if (d == 2) k_node_coords<2><<<nblk(m->ndof_cg, 256), 256, 0, s>>>(m->V, n, N, m->basis, m->X);
   else k_node_coords<3><<<nblk(m->ndof_cg, 256), 256, 0, s>>>(m->V, n, N, m->basis, m->X);
@@ -167,6 +168,88 @@ int geom_setup(lorpc_mesh* m, cudaStream_t s) {
   dfree(dbad);
   if (e != ~0ull) return fail(LORPC_ERR_INVERTED_ELEMENT, "inverted element " + std::to_string(e));
   return LORPC_OK;
+}
+
+// Gauss points of the LOR subcells (reading c2: the subcell map is multilinear in
+// the images of its corner GLL nodes; 2^d points t = 1/2 -+ 1/(2 sqrt 3)), global
+// subcell index sx + (N0-1)(sy + (N1-1) sz) major, point bits x, y, z minor.
+template <int DIM>
+__global__ void k_subcell_points(const double* __restrict__ X, int3 N, double* __restrict__ Xs) {
+  constexpr int NC = 1 << DIM;
+  const long long ns = (long long)(N.x - 1) * (N.y - 1) * (DIM == 3 ? N.z - 1 : 1);
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= ns * NC) return;
+  const long long sidx = t / NC;
+  const int ig = (int)(t % NC);
+  const int sc[3] = {(int)(sidx % (N.x - 1)), (int)((sidx / (N.x - 1)) % (N.y - 1)),
+                     DIM == 3 ? (int)(sidx / ((long long)(N.x - 1) * (N.y - 1))) : 0};
+  const double gp[2] = {0.5 - 0.5 / sqrt(3.0), 0.5 + 0.5 / sqrt(3.0)};
+  double o[3] = {0.0, 0.0, 0.0};
+  for (int c = 0; c < NC; ++c) {
+    double wv = 1.0;
+    long long id = 0, str = 1;
+    const int Nn[3] = {N.x, N.y, N.z};
+    for (int k = 0; k < DIM; ++k) {
+      const int cb = (c >> k) & 1;
+      const double tk = gp[(ig >> k) & 1];
+      wv *= cb ? tk : 1.0 - tk;
+      id += (sc[k] + cb) * str;
+      str *= Nn[k];
+    }
+    for (int i = 0; i < DIM; ++i) o[i] += wv * X[id * DIM + i];
+  }
+  for (int i = 0; i < DIM; ++i) Xs[t * DIM + i] = o[i];
+}
+
+long long n_subcells(const lorpc_mesh* m) {
+  long long n = 1;
+  for (int k = 0; k < m->d; ++k) n *= m->N[k] - 1;
+  return n;
+}
+
+int subcell_points(const lorpc_mesh* m, double* xs, cudaStream_t s) {
+  const long long tot = n_subcells(m) << m->d;
+  int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
+  if (m->d == 2) k_subcell_points<2><<<nblk(tot, 128), 128, 0, s>>>(m->X, N, xs);
+  else k_subcell_points<3><<<nblk(tot, 128), 128, 0, s>>>(m->X, N, xs);
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+
+__global__ void k_min_positive(const double* __restrict__ v, long long n, int* bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!(v[i] > 0.0)) *bad = 1;
+}
+
+// b at the volume Gauss points (K_p) and the LOR subcell Gauss points (K_h); copies
+// them, re-forms G and checks b > 0
+int set_coefficient(lorpc_mesh* m, const double* bq, const double* bs, cudaStream_t s) {
+  const long long nqt = m->nel * m->nq, nst = n_subcells(m) << m->d;
+  int* dbad = nullptr;
+  LORPC_TRY(dalloc(&dbad, 1));
+  LORPC_CUDA(cudaMemsetAsync(dbad, 0, sizeof(int), s));
+  if (bq) {
+    if (!m->bq) LORPC_TRY(dalloc(&m->bq, (size_t)nqt));
+    LORPC_CUDA(cudaMemcpyAsync(m->bq, bq, sizeof(double) * nqt, cudaMemcpyDeviceToDevice, s));
+    k_min_positive<<<296, 256, 0, s>>>(m->bq, nqt, dbad);
+    LORPC_LAUNCHED();
+  } else {
+    dfree(m->bq);
+  }
+  if (bs) {
+    if (!m->bsub) LORPC_TRY(dalloc(&m->bsub, (size_t)nst));
+    LORPC_CUDA(cudaMemcpyAsync(m->bsub, bs, sizeof(double) * nst, cudaMemcpyDeviceToDevice, s));
+    k_min_positive<<<296, 256, 0, s>>>(m->bsub, nst, dbad);
+    LORPC_LAUNCHED();
+  } else {
+    dfree(m->bsub);
+  }
+  int bad = 0;
+  LORPC_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  dfree(dbad);
+  if (bad) { dfree(m->bq); dfree(m->bsub); return fail(LORPC_ERR_ARG, "set_coefficient: b must be > 0"); }
+  return geom_setup(m, s);
 }
 
 int quad_points(const lorpc_mesh* m, double* xq, double* xbq, cudaStream_t s) {

@@ -137,21 +137,70 @@ __global__ void __launch_bounds__(128) k_mdf_ilu(MdfParams P) {
         const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
         w2[i] = mdf_w2<DIM>(At, alive, i, exist_mask<DIM>(ix, iy, iz, ex, ey, ez), ex, ey);
       }
+    if (P.ordering == 2 && lane == 0) {
+      // reverse Cuthill-McKee on the box's 3^d-stencil graph (structure only; reading
+      // r5: minimum-degree start, lowest index on ties, neighbours by (degree, index),
+      // reversed), into lev[] (free until the DAG levels are formed); cnt[] = queue,
+      // pos[] = visited marks (reset below)
+      int* q = cnt;
+      int tail = 0, head = 0;
+      while (tail < n) {
+        int s0 = -1, ds = 99;
+        for (int i = 0; i < n; ++i) {
+          if (pos[i] != -1) continue;
+          const int ix = i % ex, iy = (i / ex) % ey, iz = i / (ex * ey);
+          const int dg = __popc(exist_mask<DIM>(ix, iy, iz, ex, ey, ez)) - 1;
+          if (dg < ds) { ds = dg; s0 = i; }
+        }
+        pos[s0] = -2;
+        q[tail++] = s0;
+        while (head < tail) {
+          const int v = q[head++];
+          const int vx = v % ex, vy = (v / ex) % ey, vz = v / (ex * ey);
+          const uint32_t ev = exist_mask<DIM>(vx, vy, vz, ex, ey, ez);
+          const int t0 = tail;
+          for (int dd = 0; dd < ND; ++dd) {
+            if (dd == C || !((ev >> dd) & 1u)) continue;
+            const int u = v + doff<DIM>(dd, ex, ey);
+            if (pos[u] != -1) continue;
+            pos[u] = -2;
+            // insertion by (degree, index)
+            const int ux = u % ex, uy = (u / ex) % ey, uz = u / (ex * ey);
+            const int du = __popc(exist_mask<DIM>(ux, uy, uz, ex, ey, ez)) - 1;
+            int t = tail++;
+            while (t > t0) {
+              const int w = q[t - 1];
+              const int wx = w % ex, wy = (w / ex) % ey, wz = w / (ex * ey);
+              const int dw = __popc(exist_mask<DIM>(wx, wy, wz, ex, ey, ez)) - 1;
+              if (dw < du || (dw == du && w < u)) break;
+              q[t] = w;
+              --t;
+            }
+            q[t] = u;
+          }
+        }
+      }
+      for (int t = 0; t < n; ++t) { lev[t] = q[n - 1 - t]; pos[t] = -1; }
+    }
     __syncwarp();
     bool failed = false;
     for (int step = 0; step < n; ++step) {
       double bk = INFINITY;
       int bi = 0x7fffffff;
-      for (int i = lane; i < n; i += 32) {
-        if (!alive[i]) continue;
-        const double key = P.ordering == 0 ? q30(w2[i]) : 0.0;
-        if (key < bk || (key == bk && i < bi)) { bk = key; bi = i; }
-      }
+      if (P.ordering == 2) {
+        bi = lev[step];
+      } else {
+        for (int i = lane; i < n; i += 32) {
+          if (!alive[i]) continue;
+          const double key = P.ordering == 0 ? q30(w2[i]) : 0.0;
+          if (key < bk || (key == bk && i < bi)) { bk = key; bi = i; }
+        }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+        }
       }
       const int k = bi;
       const int kx = k % ex, ky = (k / ex) % ey, kz = k / (ex * ey);

@@ -27,7 +27,7 @@ class LorpcError(RuntimeError):
 
 
 class MeshDesc(ctypes.Structure):
-    _fields_ = [("dim", _int), ("n", _int * 3), ("p", _int), ("disc", _int), ("eta", _d)]
+    _fields_ = [("dim", _int), ("n", _int * 3), ("p", _int), ("disc", _int), ("eta", _d), ("quad", _int)]
 
 
 class SchwarzDesc(ctypes.Structure):
@@ -41,7 +41,7 @@ class PcgReport(ctypes.Structure):
 
 
 SYMBOLS = ["lorpc_mesh_create", "lorpc_mesh_destroy", "lorpc_mesh_sizes", "lorpc_quad_points",
-           "lorpc_rhs_assemble", "lorpc_operator_apply", "lorpc_lor_assemble", "lorpc_lor_destroy",
+           "lorpc_rhs_assemble", "lorpc_mesh_set_coefficient", "lorpc_subcell_points", "lorpc_operator_apply", "lorpc_lor_assemble", "lorpc_lor_destroy",
            "lorpc_schwarz_setup", "lorpc_prec_destroy", "lorpc_precond_apply",
            "lorpc_prec_export_ordering", "lorpc_prec_info", "lorpc_prec_kernel", "lorpc_prec_bytes", "lorpc_prec_profile",
            "lorpc_prec_profile_read", "lorpc_pcg_solve", "lorpc_pcg_solve_host",
@@ -69,6 +69,8 @@ def lib():
         L.lorpc_mesh_sizes.argtypes = [_vp, ctypes.POINTER(_ll), ctypes.POINTER(_ll), ctypes.POINTER(_ll)]
         L.lorpc_quad_points.argtypes = [_vp, _vp, _vp, _vp]
         L.lorpc_rhs_assemble.argtypes = [_vp, _vp, _vp, _vp, _vp]
+        L.lorpc_mesh_set_coefficient.argtypes = [_vp, _vp, _vp, _vp]
+        L.lorpc_subcell_points.argtypes = [_vp, _vp, ctypes.POINTER(_ll), _vp]
         L.lorpc_operator_apply.argtypes = [_vp, _vp, _vp, _vp]
         L.lorpc_lor_assemble.argtypes = [_vp, _vp, ctypes.POINTER(_vp)]
         L.lorpc_lor_destroy.argtypes = [_vp]
@@ -127,9 +129,9 @@ def launch_count(reset=False):
 class Mesh:
     """lorpc_mesh: Cartesian topology of multilinear tensor-product elements."""
 
-    def __init__(self, dim, n, p, vertices, disc=0, eta=0.0, stream=None):
+    def __init__(self, dim, n, p, vertices, disc=0, eta=0.0, stream=None, quad=0):
         n = list(n) + [1] * (3 - len(n))
-        self.desc = MeshDesc(dim, (_int * 3)(*n[:3]), p, disc, float(eta))
+        self.desc = MeshDesc(dim, (_int * 3)(*n[:3]), p, disc, float(eta), int(quad))
         V = np.ascontiguousarray(vertices, dtype=np.float64)
         h = _vp()
         _check(lib().lorpc_mesh_create(ctypes.byref(self.desc), V.ctypes.data, _stream(stream), ctypes.byref(h)))
@@ -146,6 +148,18 @@ class Mesh:
 
     def quad_points(self, xq=None, xbq=None, stream=None):
         _check(lib().lorpc_quad_points(self.h, _dptr(xq), _dptr(xbq), _stream(stream)))
+
+    def subcell_points(self, xs=None, stream=None):
+        """Number of LOR subcells; fills xs [n_sub * 2^d * d] with their Gauss points."""
+        n = _ll()
+        _check(lib().lorpc_subcell_points(self.h, _dptr(xs) if xs is not None else None, ctypes.byref(n),
+                                          _stream(stream)))
+        return n.value
+
+    def set_coefficient(self, bq, bsub, stream=None):
+        """b(x) at the volume Gauss points / LOR subcell Gauss points (row f3)."""
+        _check(lib().lorpc_mesh_set_coefficient(self.h, _dptr(bq) if bq is not None else None,
+                                                _dptr(bsub) if bsub is not None else None, _stream(stream)))
 
     def rhs_assemble(self, fq, gq, b, stream=None):
         _check(lib().lorpc_rhs_assemble(self.h, _dptr(fq), _dptr(gq), _dptr(b), _stream(stream)))
@@ -170,7 +184,7 @@ class Lor:
 
 
 PATCH_KIND = {"vertex": 0, "star": 1}
-ORDERING = {"mdf": 0, "natural": 1}
+ORDERING = {"mdf": 0, "natural": 1, "rcm": 2}
 COARSE = {"gmg": 0, "none": 1}
 
 
@@ -287,7 +301,7 @@ class Dist:
 
     def __init__(self, n, p, vertices, nranks, rank=0, nccl_id=None, patch_kind="vertex", ordering="mdf",
                  stream=None):
-        self.desc = MeshDesc(3, (_int * 3)(*n), p, 0, 0.0)
+        self.desc = MeshDesc(3, (_int * 3)(*n), p, 0, 0.0, 0)
         self.sdesc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], 0)
         V = np.ascontiguousarray(vertices, dtype=np.float64)
         self._id = (ctypes.c_ubyte * 128)(*nccl_id) if nccl_id is not None else None

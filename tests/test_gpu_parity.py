@@ -94,10 +94,11 @@ def _setup_both(L, cfg, ordering="mdf", coarse="gmg"):
     return mesh, lor, prec, P
 
 
+@pytest.mark.parametrize("ordering", ["mdf", "rcm"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_orderings_match_oracle(L, name):
+def test_orderings_match_oracle(L, name, ordering):
     cfg = CASES[name]
-    mesh, lor, prec, P = _setup_both(L, cfg)
+    mesh, lor, prec, P = _setup_both(L, cfg, ordering=ordering)
     assert prec.n_patches == P.npatches() and prec.n_levels == P.nlevels()
     rng = np.random.default_rng(7)
     pts = np.unique(np.concatenate([[0, prec.n_patches - 1, prec.n_patches // 2],
@@ -113,7 +114,7 @@ def test_orderings_match_oracle(L, name):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("ordering", ["mdf", "natural"])
+@pytest.mark.parametrize("ordering", ["mdf", "natural", "rcm"])
 def test_precond_parity(L, name, ordering):
     cfg = CASES[name]
     mesh, lor, prec, P = _setup_both(L, cfg, ordering=ordering)
@@ -396,3 +397,16 @@ def test_pcg_solve_host_checks_arguments(L):
         L.pcg_solve_host(mesh, prec, bo, xh, 0.0)
     with pytest.raises(L.LorpcError):
         L.pcg_solve_host(mesh, prec, bo, xh, 1e-8, maxit=0)
+
+
+@pytest.mark.parametrize("name", ["C2s", "C5s"])
+def test_rcm_pcg_parity(L, name):
+    """Row f2: RCM-ordered ILU(0) smoothing (structure-only ordering, reading r5)."""
+    cfg = CASES[name]
+    mesh, lor, prec, P = _setup_both(L, cfg, ordering="rcm")
+    bo = random_free_rhs(cfg) if cfg.rhs == "randn" else P.rhs(rhs_function(cfg, P.quad_points()))
+    x = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, cfg.tol)
+    xo, ro = P.pcg(bo, cfg.tol)
+    assert abs(rep["iters"] - ro["iters"]) <= 1
+    assert rel(x.cpu().numpy(), xo) <= 100 * cfg.tol

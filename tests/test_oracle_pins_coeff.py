@@ -127,3 +127,134 @@ def test_variable_coefficient_pcg_bounded(kind):
         _, rep = P.pcg(b, 1e-8)
         its.append(rep["iters"])
     assert its[1] <= 1.6 * its[0] and its[1] < 200, its
+
+
+# ---------------------------------------------------------------- GLL collocation (row f2 quadrature variant)
+@pytest.mark.parametrize("dim,n,p", [(2, (3, 2), 4), (3, (2, 2, 2), 3)])
+def test_gll_collocation_cartesian_kronecker(dim, n, p):
+    """Cartesian mesh: the GLL rule integrates the 1D stiffness integrand (degree
+    2p - 2) exactly but lumps the 1D mass (degree 2p) to diag(w_i h), so collocated
+    K_p = sum_j K_j (x) prod_{i != j} M^GLL_i with the exact 1D stiffness, and it
+    differs from the Gauss K_p."""
+    cfg = small_config("C3" if dim == 3 else "C1", n, p=p)
+    V = vertices(cfg)
+    Pc = O.Problem(dim, cfg.n, p, V, quad="gll")
+    from numpy.polynomial import legendre as Lg
+    xi = indep.gll_nodes(p)
+    c = np.zeros(p + 1)
+    c[p] = 1.0
+    w = 1.0 / (p * (p + 1) * Lg.legval(2 * xi - 1, c) ** 2)
+    Ks, Ml = [], []
+    for nk in cfg.n:
+        K1, _ = indep.fe_1d(p, nk)
+        h = 1.0 / nk
+        M = np.zeros(nk * p + 1)
+        for e in range(nk):
+            M[e * p:e * p + p + 1] += w * h
+        Ks.append(K1)
+        Ml.append(np.diag(M))
+    K = indep.kron_sum(Ks, Ml)
+    N = [nk * p + 1 for nk in cfg.n]
+    free = ~indep.boundary_mask(N)
+    v = np.random.default_rng(9).standard_normal(Pc.ndof)
+    v[~free] = 0.0
+    y = Pc.apply(v)
+    assert np.abs(y[free] - (K @ v)[free]).max() <= 1e-12 * np.abs(K).max()
+    yg = O.Problem(dim, cfg.n, p, V).apply(v)
+    assert np.abs(yg[free] - y[free]).max() > 1e-6 * np.abs(y).max()
+
+
+def test_gll_collocation_equals_independent_kronecker_on_perturbed():
+    """Perturbed (bilinear) mesh: the collocated operator differs from Gauss, and
+    equals sum_q w_q^GLL (J^{-T} grad l_a . J^{-T} grad l_b) detJ at the nodes,
+    recomputed here from numpy GLL weights and the vertex array."""
+    cfg = small_config("C2", (2, 2), p=3)
+    V = vertices(cfg)
+    Pc = O.Problem(2, cfg.n, 3, V, quad="gll")
+    Pg = O.Problem(2, cfg.n, 3, V)
+    xi = indep.gll_nodes(3)
+    from numpy.polynomial import legendre as Lg
+    c = np.zeros(4)
+    c[3] = 1.0
+    w = 1.0 / (3 * 4 * Lg.legval(2 * xi - 1, c) ** 2)          # GLL weights on [0,1]
+    _, D = indep.lagrange_tables(xi, xi)
+    nv = cfg.n[0] + 1
+    Vv = V.reshape(-1, 2)
+    for e in range(4):
+        ex, ey = e % 2, e // 2
+        corners = [Vv[(ex + a) + nv * (ey + b)] for b in (0, 1) for a in (0, 1)]
+        K = np.zeros((16, 16))
+        for qy in range(4):
+            for qx in range(4):
+                s, t = xi[qx], xi[qy]
+                J = (-(1 - t) * np.outer(corners[0], [1, 0]) + (1 - t) * np.outer(corners[1], [1, 0])
+                     - t * np.outer(corners[2], [1, 0]) + t * np.outer(corners[3], [1, 0])
+                     - (1 - s) * np.outer(corners[0], [0, 1]) - s * np.outer(corners[1], [0, 1])
+                     + (1 - s) * np.outer(corners[2], [0, 1]) + s * np.outer(corners[3], [0, 1]))
+                Ji = np.linalg.inv(J)
+                G = np.zeros((16, 2))
+                for a in range(16):
+                    ax, ay = a % 4, a // 4
+                    gref = np.array([D[qx, ax] * (ay == qy), (ax == qx) * D[qy, ay]])
+                    G[a] = Ji.T @ gref
+                K += w[qx] * w[qy] * np.linalg.det(J) * G @ G.T
+        assert np.abs(Pc.elem_matrix(e) - K).max() <= 1e-12 * np.abs(K).max()
+        assert np.abs(Pg.elem_matrix(e) - K).max() > 1e-8 * np.abs(K).max()
+
+
+# ---------------------------------------------------------------- RCM ordering (row f2; P:599, P:606-608)
+def _rcm_reference(A):
+    """Reading r5 written out with scipy's graph tools: BFS distances give the level
+    sets every Cuthill-McKee order must respect."""
+    import scipy.sparse.csgraph as cg
+    return cg.shortest_path(A, unweighted=True)
+
+
+def test_rcm_tridiagonal_is_reverse_path_and_exact():
+    import scipy.sparse as sp
+    n = 9
+    T = sp.diags([-1.0, 2.1, -1.0], [-1, 0, 1], shape=(n, n)).tocsr()
+    r = np.random.default_rng(4).standard_normal(n)
+    order, z = O.mdf_ilu(T, ordering=2, r=r)
+    assert list(order) == list(range(n - 1, -1, -1))     # BFS 0..n-1 from the min-degree end, reversed
+    assert np.allclose(T @ z, r, rtol=1e-13, atol=1e-13)  # no fill on a path: ILU(0) exact
+
+
+def test_rcm_visits_by_bfs_levels_and_degree():
+    """On a patch-like 27-point box graph the (reversed) RCM order visits nodes in
+    nondecreasing graph distance from its start, the start has minimum degree, and
+    among the unvisited neighbours of each node lower degree comes first."""
+    import scipy.sparse as sp
+    ex, ey, ez = 5, 4, 3
+    n = ex * ey * ez
+    rows, cols = [], []
+    for i in range(n):
+        x, y, z = i % ex, (i // ex) % ey, i // (ex * ey)
+        for dz in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    X, Y, Z = x + dx, y + dy, z + dz
+                    if 0 <= X < ex and 0 <= Y < ey and 0 <= Z < ez:
+                        rows.append(i)
+                        cols.append(X + ex * (Y + ey * Z))
+    A = sp.csr_matrix((np.where(np.array(rows) == np.array(cols), 30.0, -1.0), (rows, cols)), shape=(n, n))
+    order, _ = O.mdf_ilu(A, ordering=2)
+    cm = list(order)[::-1]
+    assert sorted(cm) == list(range(n))
+    deg = np.diff(A.indptr) - 1
+    assert deg[cm[0]] == deg.min() and cm[0] == int(np.argmin(deg))
+    dist = _rcm_reference(A)[cm[0]]
+    assert np.all(np.diff(dist[cm]) >= 0)
+
+
+@pytest.mark.parametrize("dim,n,p", [(2, (4, 4), 4), (3, (3, 3, 3), 3)])
+def test_rcm_patches_converge_like_mdf(dim, n, p):
+    """MDF- and RCM-ordered ILU give comparable iteration counts."""
+    cfg = small_config("C2" if dim == 2 else "C5", n, p=p)
+    its = {}
+    for ordering in ("mdf", "rcm"):
+        P = O.Problem(dim, cfg.n, cfg.p, vertices(cfg))
+        P.schwarz_setup("vertex", ordering, "gmg")
+        b = P.rhs(np.ones(P.quad_points().shape[0]))
+        its[ordering] = P.pcg(b, 1e-8)[1]["iters"]
+    assert abs(its["rcm"] - its["mdf"]) <= 0.3 * its["mdf"], its
