@@ -55,6 +55,8 @@ def lib():
         L.or_destroy.argtypes = [_vp]
         L.or_set_dg.argtypes = [_vp, _int, _d]
         L.or_set_quad.argtypes = [_vp, _int]
+        L.or_set_patch_extension.argtypes = [_vp, _int]
+        L.or_patch_range.argtypes = [_vp, _i64, _ip, _ip]
         L.or_ndof.restype = _i64
         L.or_ndof.argtypes = [_vp]
         L.or_elem_matrix.argtypes = [_vp, _i64, _dp]
@@ -284,7 +286,14 @@ class Problem:
         lib().or_level_csr(self.h, l, _ptr(rp, _lp), _ptr(ci, _ip), _ptr(v))
         return sp.csr_matrix((v, ci, rp), shape=(n, n))
 
-    def schwarz_setup(self, patch_kind="vertex", ordering="mdf", coarse="gmg", local_exact=False):
+    def patch_range(self, j):
+        """Element range (elo, ehi) per axis of patch j."""
+        lo, hi = np.zeros(3, dtype=np.int32), np.zeros(3, dtype=np.int32)
+        _check(lib().or_patch_range(self.h, j, _ptr(lo, _ip), _ptr(hi, _ip)))
+        return lo[:self.dim].copy(), hi[:self.dim].copy()
+
+    def schwarz_setup(self, patch_kind="vertex", ordering="mdf", coarse="gmg", local_exact=False, extend=False):
+        _check(lib().or_set_patch_extension(self.h, 1 if extend else 0))
         _check(lib().or_schwarz_setup2(self.h, PATCH_KIND[patch_kind], ORDERING[ordering], COARSE[coarse],
                                        1 if local_exact else 0))
         if self.disc != "cg":

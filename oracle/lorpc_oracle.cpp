@@ -472,6 +472,7 @@ struct Problem {
   int ordering = 0;       // 0 = MDF, 1 = natural, 2 = RCM (reading r5)
   int coarse = 0;         // 0 = GMG l1-Jacobi R_0 (reading c11), 1 = none, 2 = exact (dense)
   int local_exact = 0;    // 1: R_j = A_j^{-1} (dense Cholesky) instead of the V-cycle (pins only)
+  int extend = 0;         // 1: vertex patches extended for isotropic overlap (sec:aniso, reading r6)
   std::vector<vec> Kel;   // cached element matrices (CG) or empty
   bool cached = false;
   // LOR and hierarchy
@@ -1136,6 +1137,31 @@ static void patch_free_nodes(const Problem* P, const Patch& pt, int l, std::vect
         gid.push_back(x + (i64)Ng[0] * (y + (i64)Ng[1] * z));
 }
 
+// Patch extension for isotropic overlap (sec:aniso P:1123-1128, "patches containing
+// anisotropic elements are extended to ensure that the overlap remains isotropic";
+// rule = reading r6): along each axis, with H the largest extent of the vertex
+// patch's own elements on the vertex line through x_j, a side of the patch whose
+// physical extent from x_j is below H / 2 grows by one element layer at a time
+// (at most 4 elements per axis).
+static void extend_vertex_patch(const Mesh& m, const int* vc, Patch& pt) {
+  for (int k = 0; k < m.d; ++k) {
+    auto xk = [&](int i) {
+      int g[3] = {vc[0], vc[1], vc[2]};
+      g[k] = i;
+      const i64 vid = g[0] + (i64)m.nvx[0] * (g[1] + (i64)m.nvx[1] * g[2]);
+      return m.V[(size_t)vid * m.d + k];
+    };
+    int lo = pt.elo[k], hi = pt.ehi[k];
+    double H = 0.0;
+    for (int i = lo; i <= hi; ++i) H = std::max(H, xk(i + 1) - xk(i));
+    if (vc[k] > 0)
+      while (xk(vc[k]) - xk(lo) < 0.5 * H && lo > 0 && hi - lo + 1 < 4) --lo;
+    if (vc[k] < m.n[k])
+      while (xk(hi + 1) - xk(vc[k]) < 0.5 * H && hi < m.n[k] - 1 && hi - lo + 1 < 4) ++hi;
+    pt.elo[k] = lo; pt.ehi[k] = hi;
+  }
+}
+
 static void make_patches(Problem* P) {
   const Mesh& m = P->m;
   P->patches.clear();
@@ -1147,6 +1173,7 @@ static void make_patches(Problem* P) {
         if (k >= m.d) { pt.elo[k] = pt.ehi[k] = 0; continue; }
         pt.elo[k] = std::max(vc[k] - 1, 0); pt.ehi[k] = std::min(vc[k], m.n[k] - 1);
       }
+      if (P->extend) extend_vertex_patch(m, vc, pt);
       P->patches.push_back(pt);
     }
   } else if (P->patch_kind == 2) {  // single patch E_1 = all vertices, Omega_1 = Omega
@@ -1330,6 +1357,16 @@ extern "C" int or_schwarz_setup2(void* h, int patch_kind, int ordering, int coar
   if (!ok) { g_err = err; return 1; }
   if (coarse != 1 && !build_coarse(P)) return 1;
   P->schwarz_built = true;
+  return 0;
+}
+extern "C" int or_set_patch_extension(void* h, int extend) {
+  ((Problem*)h)->extend = extend ? 1 : 0;
+  return 0;
+}
+extern "C" int or_patch_range(void* h, i64 j, int* elo, int* ehi) {
+  const Problem* P = (const Problem*)h;
+  if (j < 0 || j >= (i64)P->patches.size()) { g_err = "patch index"; return 1; }
+  for (int k = 0; k < 3; ++k) { elo[k] = P->patches[j].elo[k]; ehi[k] = P->patches[j].ehi[k]; }
   return 0;
 }
 extern "C" int or_schwarz_setup(void* h, int patch_kind, int ordering, int coarse) {

@@ -7,5 +7,5 @@ module both `oracle/` and the product path may import.
 from .configs import CONFIGS, Config, get_config  # noqa: F401
 from .generate import (  # noqa: F401
     vertices, rhs_function, exact_solution, dirichlet_function, random_free_rhs,
-    parity_vector, small_config, coefficient_function, coefficient_b4, coefficient_samples,
+    parity_vector, small_config, coefficient_function, coefficient_b4, coefficient_samples, strip_vertices,
 )

@@ -156,3 +156,27 @@ def coefficient_samples(kind: str, cfg: Config, Xq: np.ndarray, Xs: np.ndarray):
     e = ec[0] + cfg.n[0] * (ec[1] + (cfg.n[1] * ec[2] if d == 3 else 0))
     bs = np.repeat(be[e], 1 << d)
     return bq, bs
+
+
+# ------------------------------------------------------------------ anisotropic strip meshes (row f4)
+def strip_vertices(n: int, aspect: float, row: int = None) -> np.ndarray:
+    """2D n x n Cartesian-topology mesh of [0,1]^2 whose element row `row` (default
+    n // 2) is compressed to height 1/(n aspect), so its elements have aspect ratio
+    `aspect`; the other rows share the remaining height equally (P:1107-1121,
+    sec:aniso: "a strip of high-aspect-ratio elements"; SPEC's
+    anisotropic_strip_mesh).  Vertices x-fastest, [(n+1)^2, 2]."""
+    if aspect < 1.0:
+        raise ValueError("aspect must be >= 1")
+    r = n // 2 if row is None else row
+    hs = 1.0 / (n * aspect)
+    if n > 1:
+        ho = (1.0 - hs) / (n - 1)
+        heights = np.full(n, ho)
+        heights[r] = hs
+    else:
+        heights = np.array([1.0])
+    y = np.concatenate([[0.0], np.cumsum(heights)])
+    y[-1] = 1.0
+    x = np.arange(n + 1) / n
+    X, Y = np.meshgrid(x, y, indexing="xy")
+    return np.stack([X.ravel(), Y.ravel()], axis=1)
