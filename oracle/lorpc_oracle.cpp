@@ -1381,12 +1381,20 @@ extern "C" void or_patch_ordering(void* h, i64 j, int l, int* order) {
 }
 
 // Patch V(1,1) cycle, zero initial guess, recursive over levels.
-static void patch_vcycle(const Patch& pt, int l, const vec& r, vec& z) {
+static void gmg_vcycle(const Problem* P, size_t l, const vec& r, vec& z);
+// B(1): the single patch's V-cycle has the coarse solve at its bottom —
+// its coarsest level is the p = 1 problem on T_p, solved by R_0 (one GMG V-cycle,
+// reading c11; coarse = 2: exactly) instead of the dense factor of reading c8.
+static void patch_vcycle(const Problem* P, const Patch& pt, int l, const vec& r, vec& z) {
   const PatchLevel& L = pt.lv[l];
   int n = L.n;
   z.assign(n, 0.0);
   if (n == 0) return;
-  if (L.coarsest) { z = r; chol_solve(n, L.C, z.data()); return; }
+  if (L.coarsest) {
+    if (P->patch_kind == 2 && P->coarse == 0) { gmg_vcycle(P, 0, r, z); return; }
+    if (P->patch_kind == 2 && P->coarse == 2) { z = r; if (P->n0dense) chol_solve(P->n0dense, P->C0dense, z.data()); return; }
+    z = r; chol_solve(n, L.C, z.data()); return;
+  }
   ilu_apply(L, r.data(), z.data());                          // pre-smoothing
   vec Az(n), s(n);
   L.A.matvec(z.data(), Az.data());
@@ -1396,7 +1404,7 @@ static void patch_vcycle(const Patch& pt, int l, const vec& r, vec& z) {
   for (i64 i = 0; i < Pm.nr; ++i)
     for (i64 k = Pm.rp[i]; k < Pm.rp[i + 1]; ++k) rc[Pm.ci[k]] += Pm.v[k] * s[i];
   vec ec;
-  patch_vcycle(pt, l + 1, rc, ec);
+  patch_vcycle(P, pt, l + 1, rc, ec);
   for (i64 i = 0; i < Pm.nr; ++i)
     for (i64 k = Pm.rp[i]; k < Pm.rp[i + 1]; ++k) z[i] += Pm.v[k] * ec[Pm.ci[k]];
   L.A.matvec(z.data(), Az.data());
@@ -1419,14 +1427,14 @@ static void schwarz_apply(const Problem* P, const double* r, double* z, int whic
       const PatchLevel& L0 = pt.lv[0];
       vec rj(L0.n);
       for (int i = 0; i < L0.n; ++i) rj[i] = r[L0.gid[i]];
-      patch_vcycle(pt, 0, rj, zj[j]);
+      patch_vcycle(P, pt, 0, rj, zj[j]);
     }
     for (size_t j = 0; j < P->patches.size(); ++j) {        // fixed order (a8)
       const PatchLevel& L0 = P->patches[j].lv[0];
       for (int i = 0; i < L0.n; ++i) z[L0.gid[i]] += zj[j][i];
     }
   }
-  if ((which & 2) && P->coarse != 1) {
+  if ((which & 2) && P->coarse != 1 && P->patch_kind != 2) {  // B(1): R_0 sits inside the V-cycle
     const CSR& P0 = P->P0;
     vec rcf(P0.nc, 0.0);
     for (i64 i = 0; i < P0.nr; ++i)
