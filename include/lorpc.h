@@ -69,10 +69,16 @@ typedef struct {
 
 /* Additive Schwarz B = sum_{j=0}^J R_j Q_j (eq:as P:274-277). */
 typedef struct {
-  int patch_kind; /* 0 = vertex patches (eq:patch P:302-315), 1 = element star (reading c9) */
+  int patch_kind; /* 0 = vertex patches (eq:patch P:302-315), 1 = element star (reading c9),
+                     2 = single patch B(1): one element-structured V-cycle on the whole
+                     LOR problem with R_0 at its p = 1 bottom (requires coarse = 0; levels of at
+                     most 65535 free nodes) */
   int ordering;   /* ILU(0) ordering: 0 = minimum discarded fill, 1 = natural,
                      2 = reverse Cuthill-McKee (structure only, reading r5) */
   int coarse;     /* 0 = R_0 one GMG V(1,1) with l1-Jacobi (reading c11), 1 = no coarse term */
+  int extend;     /* 1 = vertex patches extended for isotropic overlap (sec:aniso P:1123-1128,
+                     rem:anisotropy P:499-502; rule: reading r6, single rank, vertex patches
+                     only); 0 = eq:patch as is */
 } lorpc_schwarz_desc;
 
 typedef struct {

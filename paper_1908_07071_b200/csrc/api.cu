@@ -18,7 +18,7 @@ int apply_precond(const lorpc_prec* b, const double* r, double* z, cudaStream_t 
 }
 // r.z can ride on the last pass over z (the coarse prolongation) for CG with R_0
 long long rz_parts(const lorpc_prec* b) {
-  return (b->m->desc.disc == 0 && b->desc.coarse == 0) ? (b->m->ndof_cg + 255) / 256 : 0;
+  return (b->m->desc.disc == 0 && b->desc.coarse == 0 && b->desc.patch_kind != 2) ? (b->m->ndof_cg + 255) / 256 : 0;
 }
 }  // namespace lorpc
 
@@ -170,9 +170,10 @@ void lorpc_lor_destroy(lorpc_lor* l) {
 
 int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void* stream, lorpc_prec** out) {
   if (!l || !desc || !out) return fail(LORPC_ERR_ARG, "schwarz_setup: NULL argument");
-  if (desc->patch_kind < 0 || desc->patch_kind > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: patch_kind");
+  if (desc->patch_kind < 0 || desc->patch_kind > 2) return fail(LORPC_ERR_ARG, "schwarz_setup: patch_kind");
   if (desc->ordering < 0 || desc->ordering > 2) return fail(LORPC_ERR_ARG, "schwarz_setup: ordering");
   if (desc->coarse < 0 || desc->coarse > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: coarse");
+  if (desc->extend < 0 || desc->extend > 1) return fail(LORPC_ERR_ARG, "schwarz_setup: extend");
   *out = nullptr;
   lorpc_prec* b = new lorpc_prec();
   b->lor = l; b->m = l->m; b->desc = *desc;
@@ -207,7 +208,8 @@ int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void
 void lorpc_prec_destroy(lorpc_prec* b) {
   if (!b) return;
   dfree(b->rec); dfree(b->recoff); dfree(b->trec); dfree(b->trecoff); dfree(b->zpark); dfree(b->Cdi); dfree(b->pord);
-  dfree(b->wrec); dfree(b->wrecoff); dfree(b->Cq);
+  dfree(b->wrec); dfree(b->wrecoff); dfree(b->Cq); dfree(b->erng);
+  for (int l = 0; l < MAXL; ++l) { dfree(b->sgr[l]); dfree(b->sgz[l]); dfree(b->sgl[l]); dfree(b->sgw[l]); }
   for (int i = 0; i < MAXC; ++i) {
     if (i > 0) dfree(b->Ac[i]);
     dfree(b->dl1[i]); dfree(b->cr[i]); dfree(b->cz[i]); dfree(b->cs[i]);

@@ -108,6 +108,9 @@ struct lorpc_prec {
   lorpc_schwarz_desc desc;
   long long J;                      // patches
   int pvz0 = 0, pnvz = 0;           // vertex patches: planes [pvz0, pvz0 + pnvz) (0 = all; slab subsets)
+  std::vector<short> erng_h;        // extended vertex patches: element ranges [J][6] (host; empty = default)
+  short* erng = nullptr;            // the same on the device
+  int emax = 2;                     // largest number of elements of a patch along an axis
   int L;
   int max_n[lorpc::MAXL];           // largest patch size per level
   char* rec = nullptr;              // per patch-level ILU records
@@ -117,7 +120,7 @@ struct lorpc_prec {
   long long rec_max = 0;            // largest per-patch record span (bytes)
   // separable patch restriction tables: level l -> l+1, e elements along an axis
   double* wtab = nullptr;
-  int woff[lorpc::MAXL][4], wfe[lorpc::MAXL][4], wce[lorpc::MAXL][4];
+  int woff[lorpc::MAXL][5], wfe[lorpc::MAXL][5], wce[lorpc::MAXL][5];
   int scratch_doubles = 0;          // per-patch transfer scratch (V-cycle kernel)
   int Ld = 0;                       // first level replaced by the dense coarse V-cycle operator
   double* Cd = nullptr;             // [J][ldc] dense coarse operators (column-major n_Ld x n_Ld)
@@ -140,6 +143,11 @@ struct lorpc_prec {
   long long wslots = 0;
   double* Cq = nullptr;             // [wslots][378] packed dense coarse operators
   int wlp = 16;                     // lanes per patch of the W kernel (16: two patches per warp)
+  // single patch B(1) (single.cu): level-grid vectors r, z, s, w
+  double* sgr[lorpc::MAXL] = {};
+  double* sgz[lorpc::MAXL] = {};
+  double* sgl[lorpc::MAXL] = {};
+  double* sgw[lorpc::MAXL] = {};
   // coarse space (R_0)
   int nc = 0;                       // GMG levels
   int cn[lorpc::MAXC][3];           // vertices per axis

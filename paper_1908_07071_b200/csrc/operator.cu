@@ -24,13 +24,31 @@ __global__ void k_pre(const double* __restrict__ x, double* __restrict__ y, int3
   y[g] = d ? x[g] : 0.0;
 }
 
+// Q consecutive doubles from shared memory: 16-byte loads when Q is even (every read
+// below starts at a multiple of Q doubles of a 16-byte-aligned array)
+template <int Q>
+__device__ __forceinline__ void lds_vec(const double* p, double (&v)[Q]) {
+  if constexpr (Q % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < Q / 2; ++i) {
+      const double2 t = reinterpret_cast<const double2*>(p)[i];
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = p[i];
+  }
+}
+
 template <int P, int EB>
 __global__ void __launch_bounds__((P + 1) * (P + 1) * EB)
 k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ G, int3 n, int3 N,
       Basis1D bs, long long e0, long long e1) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q * Q * Q;
   __shared__ double sB[Q2], sD[Q2];
-  __shared__ double S[EB][3][Q3];
+  // stage layouts: every contraction reads its Q operands contiguously (lds_vec)
+  __shared__ __align__(16) double S[EB][3][Q3];
   const int tx = threadIdx.x, ty = threadIdx.y, te = threadIdx.z;
   const int lt = tx + Q * (ty + Q * te);
   for (int i = lt; i < Q2; i += Q2 * EB) { sB[i] = bs.B[i]; sD[i] = bs.D[i]; }
@@ -59,19 +77,20 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
     double bu = 0.0, du = 0.0;
 #pragma unroll
     for (int c = 0; c < Q; ++c) { bu += sB[qz * Q + c] * u[c]; du += sD[qz * Q + c] * u[c]; }
-    S0[qz * Q2 + ty * Q + tx] = bu;  // [qz][b][a]
-    S1[qz * Q2 + ty * Q + tx] = du;
+    S0[qz * Q2 + tx * Q + ty] = bu;  // [qz][a][b]
+    S1[qz * Q2 + tx * Q + ty] = du;
   }
   __syncthreads();
   // y contraction: thread (a = tx, qy = ty)
   double r1[Q], r2[Q], r3[Q];
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
-    double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+    double t1 = 0.0, t2 = 0.0, t3 = 0.0, v0[Q], v1[Q];
+    lds_vec<Q>(S0 + qz * Q2 + tx * Q, v0);
+    lds_vec<Q>(S1 + qz * Q2 + tx * Q, v1);
 #pragma unroll
     for (int b = 0; b < Q; ++b) {
-      const double s0 = S0[qz * Q2 + b * Q + tx], s1 = S1[qz * Q2 + b * Q + tx];
-      t1 += sB[ty * Q + b] * s0; t2 += sD[ty * Q + b] * s0; t3 += sB[ty * Q + b] * s1;
+      t1 += sB[ty * Q + b] * v0[b]; t2 += sD[ty * Q + b] * v0[b]; t3 += sB[ty * Q + b] * v1[b];
     }
     r1[qz] = t1; r2[qz] = t2; r3[qz] = t3;
   }
@@ -85,12 +104,15 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
   const double* Ge = G + (active ? e : 0) * 6 * Q3;
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
-    double gxv = 0.0, gyv = 0.0, gzv = 0.0;
+    double gxv = 0.0, gyv = 0.0, gzv = 0.0, v0[Q], v1[Q], v2[Q];
+    lds_vec<Q>(S0 + qz * Q2 + ty * Q, v0);
+    lds_vec<Q>(S1 + qz * Q2 + ty * Q, v1);
+    lds_vec<Q>(S2 + qz * Q2 + ty * Q, v2);
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
-      gxv += sD[tx * Q + a] * S0[qz * Q2 + ty * Q + a];
-      gyv += sB[tx * Q + a] * S1[qz * Q2 + ty * Q + a];
-      gzv += sB[tx * Q + a] * S2[qz * Q2 + ty * Q + a];
+      gxv += sD[tx * Q + a] * v0[a];
+      gyv += sB[tx * Q + a] * v1[a];
+      gzv += sB[tx * Q + a] * v2[a];
     }
     const int iq = tx + Q * (ty + Q * qz);
     const double g00 = Ge[0 * Q3 + iq], g01 = Ge[1 * Q3 + iq], g02 = Ge[2 * Q3 + iq];
@@ -108,30 +130,36 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
   // x^T: thread (a = tx, qy = ty)
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
-    double w1 = 0.0, w2 = 0.0, w3 = 0.0;
+    double w1 = 0.0, w2 = 0.0, w3 = 0.0, v0[Q], v1[Q], v2[Q];
+    lds_vec<Q>(S0 + qz * Q2 + ty * Q, v0);
+    lds_vec<Q>(S1 + qz * Q2 + ty * Q, v1);
+    lds_vec<Q>(S2 + qz * Q2 + ty * Q, v2);
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
-      w1 += sD[qx * Q + tx] * S0[qz * Q2 + ty * Q + qx];
-      w2 += sB[qx * Q + tx] * S1[qz * Q2 + ty * Q + qx];
-      w3 += sB[qx * Q + tx] * S2[qz * Q2 + ty * Q + qx];
+      w1 += sD[qx * Q + tx] * v0[qx];
+      w2 += sB[qx * Q + tx] * v1[qx];
+      w3 += sB[qx * Q + tx] * v2[qx];
     }
     r1[qz] = w1; r2[qz] = w2; r3[qz] = w3;
   }
   __syncthreads();
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    S0[qz * Q2 + ty * Q + tx] = r1[qz]; S1[qz * Q2 + ty * Q + tx] = r2[qz]; S2[qz * Q2 + ty * Q + tx] = r3[qz];
+  for (int qz = 0; qz < Q; ++qz) {  // [qz][a][qy]
+    S0[qz * Q2 + tx * Q + ty] = r1[qz]; S1[qz * Q2 + tx * Q + ty] = r2[qz]; S2[qz * Q2 + tx * Q + ty] = r3[qz];
   }
   __syncthreads();
   // y^T: thread (a = tx, b = ty) -> YB (then B_z^T), YD (then D_z^T)
   double yb[Q], yd[Q];
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
-    double t1 = 0.0, t2 = 0.0;
+    double t1 = 0.0, t2 = 0.0, v0[Q], v1[Q], v2[Q];
+    lds_vec<Q>(S0 + qz * Q2 + tx * Q, v0);
+    lds_vec<Q>(S1 + qz * Q2 + tx * Q, v1);
+    lds_vec<Q>(S2 + qz * Q2 + tx * Q, v2);
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
-      t1 += sB[qy * Q + ty] * S0[qz * Q2 + qy * Q + tx] + sD[qy * Q + ty] * S1[qz * Q2 + qy * Q + tx];
-      t2 += sB[qy * Q + ty] * S2[qz * Q2 + qy * Q + tx];
+      t1 += sB[qy * Q + ty] * v0[qy] + sD[qy * Q + ty] * v1[qy];
+      t2 += sB[qy * Q + ty] * v2[qy];
     }
     yb[qz] = t1; yd[qz] = t2;
   }

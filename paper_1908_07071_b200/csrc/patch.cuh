@@ -7,15 +7,25 @@ namespace lorpc {
 
 // ------------------------------------------------------------------ patch geometry
 struct PatchGeom {
-  int d, kind;          // kind 0 vertex, 1 star
+  int d, kind;          // kind 0 vertex, 1 star, 2 single patch (B(1))
   int n[3];             // elements per axis
   int ml[MAXL];         // nodes per element per axis at each level
   int Nax[MAXL][3];     // level grid per axis
   int L;
   int vz0;              // vertex patches: z index of the first patch plane (slab subsets)
+  const short* erng;    // per patch element ranges {elo0, ehi0, elo1, ehi1, elo2, ehi2} (extended
+                        // vertex patches, reading r6) or nullptr (default ranges)
 };
 
 __host__ __device__ __forceinline__ void patch_elems(const PatchGeom& G, long long j, int* elo, int* ehi) {
+  if (G.erng) {
+    for (int k = 0; k < 3; ++k) { elo[k] = G.erng[6 * j + 2 * k]; ehi[k] = G.erng[6 * j + 2 * k + 1]; }
+    return;
+  }
+  if (G.kind == 2) {  // single patch B(1): the whole domain
+    for (int k = 0; k < 3; ++k) { elo[k] = 0; ehi[k] = k < G.d ? G.n[k] - 1 : 0; }
+    return;
+  }
   if (G.kind == 0) {
     const long long nv0 = G.n[0] + 1, nv1 = G.n[1] + 1;
     const int v[3] = {(int)(j % nv0), (int)((j / nv0) % nv1), (int)(j / (nv0 * nv1)) + G.vz0};

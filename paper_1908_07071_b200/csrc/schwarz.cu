@@ -33,6 +33,7 @@ int dense_coarse_setup(lorpc_prec* b, cudaStream_t s);  // vcycle.cu
 int trec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_t.cu
 size_t tmode_smem(const lorpc_prec* b);
 int wrec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_w.cu
+int single_setup(lorpc_prec* b);                        // single.cu
 size_t wmode_smem(const lorpc_prec* b);
 
 // ------------------------------------------------------------------ MDF + ILU(0)
@@ -360,6 +361,7 @@ PatchGeom make_geom(const lorpc_prec* b) {
   PatchGeom G{};
   const lorpc_mesh* m = b->m;
   G.d = m->d; G.kind = b->desc.patch_kind; G.L = b->lor->L; G.vz0 = b->pvz0;
+  G.erng = b->erng;
   for (int k = 0; k < 3; ++k) G.n[k] = m->n[k];
   for (int l = 0; l < G.L; ++l) {
     G.ml[l] = b->lor->ml[l];
@@ -487,10 +489,53 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
     if (b->pnvz <= 0) { b->pvz0 = 0; b->pnvz = nvz; }
     if (b->pvz0 < 0 || b->pvz0 + b->pnvz > nvz) return fail(LORPC_ERR_ARG, "schwarz: patch plane range");
     b->J = (long long)(m->n[0] + 1) * (m->n[1] + 1) * b->pnvz;
+  } else if (b->desc.patch_kind == 2) {
+    if (b->desc.coarse != 0) return fail(LORPC_ERR_ARG, "schwarz: B(1) needs R_0 (coarse = 0) at its bottom");
+    b->pvz0 = 0; b->pnvz = 0;
+    b->J = 1;
   } else {
     b->pvz0 = 0; b->pnvz = 0;
     b->J = m->nel;
   }
+  // extended vertex patches (sec:aniso P:1123-1128, reading r6): along each axis, a
+  // side of the patch shorter than half of the largest of its own elements on the
+  // vertex line through x_j grows by one element layer at a time, <= 4 elements
+  b->emax = b->desc.patch_kind == 0 ? 2 : 3;
+  if (b->desc.extend) {
+    if (b->desc.patch_kind != 0) return fail(LORPC_ERR_ARG, "schwarz: patch extension needs vertex patches");
+    if (b->pnvz != (d == 3 ? m->n[2] + 1 : 1) || b->pvz0 != 0)
+      return fail(LORPC_ERR_ARG, "schwarz: patch extension is single-rank only");
+    const int nv[3] = {m->n[0] + 1, m->n[1] + 1, d == 3 ? m->n[2] + 1 : 1};
+    std::vector<double> V((size_t)nv[0] * nv[1] * nv[2] * d);
+    LORPC_CUDA(cudaMemcpy(V.data(), m->V, sizeof(double) * V.size(), cudaMemcpyDeviceToHost));
+    b->erng_h.assign((size_t)b->J * 6, 0);
+    b->emax = 1;
+    for (long long j = 0; j < b->J; ++j) {
+      const int vc[3] = {(int)(j % nv[0]), (int)((j / nv[0]) % nv[1]), (int)(j / ((long long)nv[0] * nv[1]))};
+      for (int k = 0; k < d; ++k) {
+        auto xk = [&](int i) {
+          int g[3] = {vc[0], vc[1], vc[2]};
+          g[k] = i;
+          return V[((size_t)g[0] + (size_t)nv[0] * (g[1] + (size_t)nv[1] * g[2])) * d + k];
+        };
+        int lo = std::max(vc[k] - 1, 0), hi = std::min(vc[k], m->n[k] - 1);
+        double H = 0.0;
+        for (int i = lo; i <= hi; ++i) H = std::max(H, xk(i + 1) - xk(i));
+        if (vc[k] > 0)
+          while (xk(vc[k]) - xk(lo) < 0.5 * H && lo > 0 && hi - lo + 1 < 4) --lo;
+        if (vc[k] < m->n[k])
+          while (xk(hi + 1) - xk(vc[k]) < 0.5 * H && hi < m->n[k] - 1 && hi - lo + 1 < 4) ++hi;
+        b->erng_h[6 * j + 2 * k] = (short)lo;
+        b->erng_h[6 * j + 2 * k + 1] = (short)hi;
+        b->emax = std::max(b->emax, hi - lo + 1);
+      }
+    }
+    LORPC_TRY(dalloc(&b->erng, b->erng_h.size()));
+    LORPC_CUDA(cudaMemcpy(b->erng, b->erng_h.data(), sizeof(short) * b->erng_h.size(), cudaMemcpyHostToDevice));
+    G.erng = b->erng;
+  }
+  PatchGeom Gh = G;  // host copy of the geometry for the record sizes
+  if (b->desc.extend) Gh.erng = b->erng_h.data();
   // record offsets (host; patch sizes are index arithmetic)
   b->recoff_h.assign((size_t)b->J * L, 0);
   long long off = 0;
@@ -500,7 +545,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
     const long long start = off;
     for (int l = 0; l < L; ++l) {
       int lo[3], ext[3];
-      patch_box(G, j, l, lo, ext);
+      patch_box(Gh, j, l, lo, ext);
       const int n = std::max(ext[0] * ext[1] * ext[2], 0);
       if (n > 65535) return fail(LORPC_ERR_SIZE, "patch too large");
       if (num_edges(d, ext) > 65535)  // record row offsets (frp / brp) are u16
@@ -556,13 +601,13 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   // elements along the axis: W[ic][f] = P_l(f, ic) on the free nodes of e elements.
   {
     std::vector<double> W;
-    int emax = b->desc.patch_kind == 0 ? 2 : 3;
+    const int emax = b->emax;
     b->scratch_doubles = 0;
     for (int l = 0; l + 1 < L; ++l) {
       const Transfer1D& T = lor->T[l];
       const int mf = lor->ml[l], mc = lor->ml[l + 1];
-      for (int e = 0; e < 4; ++e) { b->woff[l][e] = 0; b->wfe[l][e] = 0; b->wce[l][e] = 0; }
-      for (int e = 1; e <= 3; ++e) {
+      for (int e = 0; e < 5; ++e) { b->woff[l][e] = 0; b->wfe[l][e] = 0; b->wce[l][e] = 0; }
+      for (int e = 1; e <= 4; ++e) {
         const int fe = e * (mf - 1) - 1, ce = e * (mc - 1) - 1;
         b->woff[l][e] = (int)W.size(); b->wfe[l][e] = fe; b->wce[l][e] = ce;
         W.resize(W.size() + (size_t)std::max(fe * ce, 0), 0.0);
@@ -600,6 +645,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
     const int nv[3] = {m->n[0] + 1, m->n[1] + 1, d == 3 ? m->n[2] + 1 : 1};
     LORPC_TRY(gmg_build(b, lor->A[L - 1], nv, d, s));
   }
+  if (b->desc.patch_kind == 2) return single_setup(b);  // B(1): level-grid V-cycle (single.cu)
   // dense coarse V-cycle operators: first level l >= 1 with <= 32 free nodes per patch
   // (the coarsest level if none); the V-cycle below it is one symmetric matrix
   b->Ld = L - 1;
@@ -617,7 +663,8 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
     // opt-in (LORPC_WMODE=1): parity-exact, but measured slower than the thread-mode
     // kernels on C5: only ~14 patches fit per SM with their factor
     // resident, and the push-round chains are latency-bound
-    const bool eligible = d == 3 && b->desc.patch_kind == 0 && b->Ld == 1 && cx <= 3 && b->max_n[0] <= 255;
+    const bool eligible = d == 3 && b->desc.patch_kind == 0 && !b->desc.extend && b->Ld == 1 && cx <= 3 &&
+                          b->max_n[0] <= 255;
     const char* e = getenv("LORPC_WMODE");
     b->wmode = eligible && e && atoi(e) != 0;
     if (b->wmode) {
@@ -628,7 +675,7 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
   }
   // thread-per-patch V-cycle when the warp's 32 patch vectors fit in shared memory
   // (level-1 boxes of at most 3 (3D) / 5 (2D) nodes per axis, see vcycle_t.cu TCoarse)
-  const int cext_max = (b->desc.patch_kind == 0 ? 2 : 3) * (lor->ml[1] - 1) - 1;
+  const int cext_max = b->emax * (lor->ml[1] - 1) - 1;
   b->tmode = b->Ld == 1 && b->max_n[1] <= 32 && cext_max <= (d == 3 ? 3 : 5) && tmode_smem(b) <= 227 * 1024 &&
              b->max_n[0] <= 65534;
   if (const char* e = getenv("LORPC_TMODE")) b->tmode = b->tmode && atoi(e) != 0;

@@ -211,7 +211,7 @@ struct VcParams {
   PatchGeom G;
   const double* A[MAXL];
   const double* W;        // separable 1D restriction tables (host-built, see schwarz.cu)
-  int woff[MAXL][4];      // table offset for (level l -> l+1, elements along the axis 1..3)
+  int woff[MAXL][5];      // table offset for (level l -> l+1, elements along the axis 1..4)
   const char* rec;
   const long long* recoff;
   long long J;
@@ -665,9 +665,15 @@ int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaS
   return b->m->d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
 }
 
+int single_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);  // single.cu
+
 int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream_t s, double* rzpart) {
   const lorpc_mesh* m = b->m;
   const int d = m->d;
+  if (b->desc.patch_kind == 2) {  // B(1): R_0 at the bottom of the one V-cycle, no additive term
+    if (rzpart) return fail(LORPC_ERR_ARG, "schwarz_apply_cg: fused r.z needs the additive coarse term");
+    return single_apply(b, r, z, s);
+  }
   const bool coarse = b->desc.coarse == 0;
   const double* z0 = nullptr;
   // R_0 concurrently with the patch batch on the aux stream is opt-in (LORPC_OVERLAP=1):

@@ -267,7 +267,7 @@ struct TcParams {
   PatchGeom G;
   const double* A0;  // finest LOR level, node-major rows of NDP doubles
   const double* W;   // separable restriction tables, level 0 -> 1
-  int woff[4];
+  int woff[5];
   const char* trec;
   const long long* trecoff;
   const int* pord;

@@ -264,7 +264,7 @@ struct WParams {
   PatchGeom G;
   const double* A0;           // finest LOR level, node-major rows of 28 doubles
   const double* W;            // separable restriction tables, level 0 -> 1
-  int woff[4];
+  int woff[5];
   const char* wrec;
   const long long* wrecoff;   // [nslots + 1]
   const int* pord;

@@ -31,7 +31,7 @@ class MeshDesc(ctypes.Structure):
 
 
 class SchwarzDesc(ctypes.Structure):
-    _fields_ = [("patch_kind", _int), ("ordering", _int), ("coarse", _int)]
+    _fields_ = [("patch_kind", _int), ("ordering", _int), ("coarse", _int), ("extend", _int)]
 
 
 class PcgReport(ctypes.Structure):
@@ -183,7 +183,7 @@ class Lor:
             self.h = None
 
 
-PATCH_KIND = {"vertex": 0, "star": 1}
+PATCH_KIND = {"vertex": 0, "star": 1, "single": 2}
 ORDERING = {"mdf": 0, "natural": 1, "rcm": 2}
 COARSE = {"gmg": 0, "none": 1}
 
@@ -191,10 +191,10 @@ COARSE = {"gmg": 0, "none": 1}
 class Prec:
     """lorpc_prec: additive Schwarz B (eq:as) or B_DG (eq:dg-as)."""
 
-    def __init__(self, lor, patch_kind="vertex", ordering="mdf", coarse="gmg", stream=None):
+    def __init__(self, lor, patch_kind="vertex", ordering="mdf", coarse="gmg", stream=None, extend=False):
         self.lor = lor
         self.mesh = lor.mesh
-        self.desc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], COARSE[coarse])
+        self.desc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], COARSE[coarse], 1 if extend else 0)
         h = _vp()
         _check(lib().lorpc_schwarz_setup(lor.h, ctypes.byref(self.desc), _stream(stream), ctypes.byref(h)))
         self.h = h
@@ -302,7 +302,7 @@ class Dist:
     def __init__(self, n, p, vertices, nranks, rank=0, nccl_id=None, patch_kind="vertex", ordering="mdf",
                  stream=None):
         self.desc = MeshDesc(3, (_int * 3)(*n), p, 0, 0.0, 0)
-        self.sdesc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], 0)
+        self.sdesc = SchwarzDesc(PATCH_KIND[patch_kind], ORDERING[ordering], 0, 0)
         V = np.ascontiguousarray(vertices, dtype=np.float64)
         self._id = (ctypes.c_ubyte * 128)(*nccl_id) if nccl_id is not None else None
         h = _vp()

@@ -127,3 +127,32 @@ def test_gll_collocation_rejects_dg(L):
     c4 = small_config("C4", (2, 2, 2), p=2)
     with pytest.raises(L.LorpcError):
         L.Mesh(3, c4.n, c4.p, vertices(c4), disc=1, eta=90.0, quad=1)
+
+
+# ---------------------------------------------------------------- B(1) single patch (row f2)
+@pytest.mark.parametrize("ordering", ["mdf", "rcm"])
+@pytest.mark.parametrize("cfg", [small_config("C1", (4, 4), p=3), small_config("C2", (6, 5), p=5),
+                                 small_config("C5", (3, 2, 3), p=3)], ids=["2Dcart", "2Dpert", "3Dpert"])
+def test_single_patch_b1_parity(L, cfg, ordering):
+    """B(1): one element-structured V-cycle on the whole LOR problem, ILU(0)
+    smoothing per level, R_0 at the p = 1 bottom.  Preconditioner element-wise and PCG
+    against the oracle's single patch kind."""
+    V = vertices(cfg)
+    mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, V)
+    prec = L.Prec(L.Lor(mesh), patch_kind="single", ordering=ordering)
+    P = O.Problem(cfg.dim, cfg.n, cfg.p, V)
+    P.schwarz_setup("single", ordering, "gmg")
+    r = parity_vector(P.ndof, seed=55)
+    X = P.node_coords()
+    r[~np.all((X > 1e-12) & (X < 1 - 1e-12), axis=1)] = 0.0
+    z = torch.empty(mesh.n_dof, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z)
+    zo = P.precond(r)
+    assert rel(z.cpu().numpy(), zo) <= TOL
+    assert np.abs(z.cpu().numpy() - zo).max() <= TOL * np.abs(zo).max()
+    bo = P.rhs(np.ones(P.quad_points().shape[0]))
+    x = torch.empty_like(z)
+    rep = L.pcg_solve(mesh, prec, dev(bo), x, 1e-10)
+    xo, ro = P.pcg(bo, 1e-10)
+    assert iters_match(P, bo, 1e-10, rep["iters"], ro["iters"]), (rep["iters"], ro["iters"])
+    assert rel(x.cpu().numpy(), xo) <= 1e-8

@@ -1,0 +1,19 @@
+# Round-2 measurement pass on one B200 (run under gpurun): bench lines for C5
+# (headline), C4 (three SIPG solves), C3, C2; launch list of one C5 step; ncu full
+# capture of the C5 V-cycle kernels and the operator (C5 recipe, 64^3).
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+python bench.py --steps 5 --warmup 3 > gpurun_out/r02_bench_C5.json 2> gpurun_out/r02_bench_C5.err; echo "C5 rc=$?"
+for c in C4 C3 C2; do
+  python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/r02_bench_$c.json 2> gpurun_out/r02_bench_$c.err
+  echo "$c rc=$?"
+done
+python tools/prof_prec.py C5 2 > gpurun_out/prof_prec_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:"k_vt|k_cg3|k_dot|k_update|k_prolong|k_restrict|k_jacobi|k_residual|k_coarsest|k_pre" \
+    -c 40 --csv --log-file gpurun_out/r02_launches_C5.csv python tools/prof_prec.py C5 2 > gpurun_out/ncu_l.log 2>&1
+echo "launch list rc=$?"
+python tools/prof_prec.py C5m 2 > gpurun_out/prof_prec_plain_m.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_vt|k_cg3" -s 0 -c 4 \
+    -o gpurun_out/r02_prof_C5m -f python tools/prof_prec.py C5m 1 > gpurun_out/ncu_full.log 2>&1
+echo "ncu full rc=$?"
