@@ -113,3 +113,41 @@ def test_dist_nccl_single_rank(L):
     repd = D.pcg_solve([dev(b)], [xd], cfg.tol)
     assert repd["iters"] == rep1["iters"]
     assert rel(xd.cpu().numpy(), x1.cpu().numpy()) < 1e-12
+
+
+def test_dist_eight_ranks_c5_recipe_32cubed(L):
+    """R = 8 emulated ranks of four element layers each on the C5 recipe at 32^3 (the
+    8-GPU slab shape at 1/64 of the volume): operator and preconditioner equal the
+    single-rank path to 1e-12, PCG iterations +-1 and the solution 1e-9 (the single-rank
+    path itself is checked against the oracle at this size in test_gpu_large.py)."""
+    cfg = small_config("C5", (32, 32, 32), p=3)
+    V = vertices(cfg)
+    mesh = L.Mesh(3, cfg.n, 3, V)
+    prec = L.Prec(L.Lor(mesh))
+    D = L.Dist(cfg.n, 3, V, 8)
+    N = mesh.n_dof
+    x = parity_vector(N, seed=56)
+    y1 = torch.empty(N, dtype=torch.float64, device="cuda")
+    mesh.apply(dev(x), y1)
+    ys = [torch.empty_like(t) for t in split(D, x)]
+    D.apply(split(D, x), ys)
+    torch.cuda.synchronize()
+    assert rel(join(D, ys, N), y1.cpu().numpy()) < 1e-12
+    g = np.arange(N)
+    Nx = cfg.n[0] * 3 + 1
+    ix, iy, iz = g % Nx, (g // Nx) % Nx, g // (Nx * Nx)
+    r = x.copy()
+    r[(ix == 0) | (ix == Nx - 1) | (iy == 0) | (iy == Nx - 1) | (iz == 0) | (iz == Nx - 1)] = 0.0
+    z1 = torch.empty(N, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z1)
+    zs = [torch.empty_like(t) for t in split(D, r)]
+    D.precond(split(D, r), zs)
+    torch.cuda.synchronize()
+    assert rel(join(D, zs, N), z1.cpu().numpy()) < 1e-12
+    b = random_free_rhs(cfg)
+    x1 = torch.empty(N, dtype=torch.float64, device="cuda")
+    rep1 = L.pcg_solve(mesh, prec, dev(b), x1, cfg.tol)
+    xs = [torch.empty_like(t) for t in split(D, b)]
+    repd = D.pcg_solve(split(D, b), xs, cfg.tol)
+    assert abs(repd["iters"] - rep1["iters"]) <= 1, (repd["iters"], rep1["iters"])
+    assert rel(join(D, xs, N), x1.cpu().numpy()) < 1e-9
