@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--config", default=HEADLINE)
     ap.add_argument("--impl", default="lorpc", choices=["lorpc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ordering", default=None, choices=["mdf", "rcm", "natural"],
+                    help="ILU(0) ordering of the patch smoothers (default: ORDERING[config])")
     return ap.parse_args()
 
 
@@ -95,7 +97,7 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle sample
-def oracle_sample(cfg_name, reps=1):
+def oracle_sample(cfg_name, reps=1, ordering="mdf"):
     """Time the oracle (test infrastructure, never tuned) on a bounded sample of the
     headline workload: same recipe, smaller mesh; full PCG solve, setup excluded."""
     import oracle as O
@@ -103,7 +105,7 @@ def oracle_sample(cfg_name, reps=1):
     cfg = small_config(cfg_name, CPU_SAMPLE[cfg_name])
     P = O.Problem.from_config(cfg)
     b = random_free_rhs(cfg) if cfg.rhs == "randn" else P.rhs(rhs_function(cfg, P.quad_points()))
-    P.schwarz_setup(cfg.patch_kind, "mdf", "gmg")
+    P.schwarz_setup(cfg.patch_kind, ordering, "gmg")
     P.apply(b)  # element-matrix cache built outside the timed region (setup)
     t = 0.0
     iters = 0
@@ -115,7 +117,8 @@ def oracle_sample(cfg_name, reps=1):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
     return {"value": P.ndof * iters / t, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{cfg.name}: {cfg_name} recipe (p={cfg.p}, same perturbation/seeds/RHS kind) on "
-                      f"{'x'.join(map(str, cfg.n))} elements, n_dof={P.ndof}, full PCG solve to tol={cfg.tol} "
+                      f"{'x'.join(map(str, cfg.n))} elements, n_dof={P.ndof}, {ordering.upper()}-ILU(0), "
+                      f"full PCG solve to tol={cfg.tol} "
                       f"({iters // reps} iterations), setup excluded, {reps} solve(s), {t:.1f} s"}, t
 
 
@@ -124,10 +127,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     for _ in range(args.warmup):
-        oracle_sample(args.config)
+        oracle_sample(args.config, ordering=args.ordering)
     vals, ts = [], []
     for _ in range(args.steps):
-        cb, t = oracle_sample(args.config)
+        cb, t = oracle_sample(args.config, ordering=args.ordering)
         vals.append(cb["value"])
         ts.append(t)
     value = statistics.mean(vals)
@@ -168,7 +171,7 @@ def run_lorpc(args):
     if world > 1 or force_dist:
         return run_lorpc_dist(args, cfg, dev, rank, world, dist)
     t0 = time.perf_counter()
-    probs = build_problems(L, cfg, dev)
+    probs = build_problems(L, cfg, dev, args.ordering)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
 
@@ -264,7 +267,7 @@ def run_lorpc(args):
     per_launch_ms = vc_ms / max(vc_n, 1)
     achieved = vc_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.ordering}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("k_vcycle_bytes_per_launch")
     working_set = vc_bytes + 40 * n_dof
@@ -287,7 +290,8 @@ def run_lorpc(args):
             "data": "synthetic (seeded workloads/ generators)",
             "config": {"workload": f"{cfg.name}: {cfg.dim}D {disc} {'x'.join(map(str, cfg.n))} "
                                    f"p={cfg.p}, perturb={cfg.perturb}h, {cfg.patch_kind} patches, "
-                                   f"MDF-ILU(0) V(1,1), GMG R_0{pens}, tol={cfg.tol}",
+                                   f"{args.ordering.upper()}-ILU(0) V(1,1), GMG R_0{pens}, tol={cfg.tol}",
+                       "ordering": args.ordering,
                        "n_dof": n_dof, "pcg_iters_per_solve": iters[0], "n_patches": prec0.n_patches,
                        "setup_s": round(t_setup, 3), "parallelism": "replicas" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (working set >> 126 MB)" if working_set > 4 * 126e6
@@ -309,7 +313,7 @@ def run_lorpc(args):
                     "d2h_bytes_per_step": 8 * n_dof * len(probs)},
             "gpu_launches": launches, "clocks": ck}
     if world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE:
-        cb, _ = oracle_sample(args.config)
+        cb, _ = oracle_sample(args.config, ordering=args.ordering)
         line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     if dist:
@@ -317,7 +321,7 @@ def run_lorpc(args):
     return 0
 
 
-def build_problems(L, cfg, dev):
+def build_problems(L, cfg, dev, ordering="mdf"):
     """The config's solves: one for CG configs, one per penalty for SIPG (C4)."""
     import torch
     from workloads import dirichlet_function, random_free_rhs, rhs_function, vertices
@@ -330,7 +334,7 @@ def build_problems(L, cfg, dev):
         else:
             mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, V, disc=1, eta=eta)
         lor = L.Lor(mesh)
-        prec = L.Prec(lor, patch_kind=cfg.patch_kind)
+        prec = L.Prec(lor, patch_kind=cfg.patch_kind, ordering=ordering)
         if cfg.rhs == "randn":
             b_host = random_free_rhs(cfg)
             b = torch.from_numpy(b_host).to(dev)
@@ -458,8 +462,14 @@ def run_lorpc_dist(args, cfg, dev, rank, world, dist):
     return 0
 
 
+# ILU(0) ordering per config when --ordering is not given
+ORDERING = {"C1": "mdf", "C2": "mdf", "C3": "mdf", "C4": "mdf", "C5": "mdf"}
+
+
 def main():
     args = parse()
+    if args.ordering is None:
+        args.ordering = ORDERING.get(args.config, "mdf")
     if args.impl == "reference":
         return run_reference(args)
     return run_lorpc(args)

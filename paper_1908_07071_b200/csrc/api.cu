@@ -246,7 +246,7 @@ int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels) {
 
 int lorpc_prec_kernel(const lorpc_prec* b, int* mode) {
   if (!b || !mode) return fail(LORPC_ERR_ARG, "prec_kernel: NULL");
-  *mode = b->wmode ? 2 : b->tmode ? 1 : 0;
+  *mode = b->wmode ? 2 : b->umode ? 3 : b->tmode ? 1 : 0;
   return LORPC_OK;
 }
 

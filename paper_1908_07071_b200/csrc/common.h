@@ -128,6 +128,8 @@ struct lorpc_prec {
   int lanes = 8;                    // lanes per patch in the V-cycle kernel
   // thread-per-patch V-cycle (vcycle_t.cu): warp-interleaved factors, parking buffer
   bool tmode = false;
+  bool umode = false;               // thread mode with one shared sweep schedule per warp (U-records)
+  long long tslots = 0;             // warp slots of pord (multiple of 32)
   char* trec = nullptr;
   long long* trecoff = nullptr;
   long long trec_bytes = 0;

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include "patch.cuh"
@@ -215,14 +216,178 @@ __global__ void k_pack_c(const double* __restrict__ Cd, double* __restrict__ Cp,
   Cp[t] = v;
 }
 
+// ------------------------------------------------------------------ U-records
+// Structure-only orderings (natural, RCM = reading r5) give every patch with the
+// same free-node box the same elimination order and the same factor sparsity, so
+// the 32 patches of a warp (grouped by box shape) share ONE sweep schedule.  The
+// U-record stores that schedule once, as a 32-byte descriptor per step read
+// warp-uniformly, and per lane only the factor VALUES: no per-lane node indices or
+// headers and no padding to the warp's widest column (T-records), i.e. the L and
+// D of the factor plus at most one zero entry per odd column.  P:606-608: "MDF-
+// ordered and RCM-ordered ILU give comparable iteration counts".
+// Block of warp w at trecoff[w], 256-byte aligned:
+//   int4 {S, E2, 0, 0}: S steps, E2 pair rows
+//   desc[S]     32 B: node k (byte 0), pair rows mp (byte 1), first pair row kp
+//               (bytes 2-3, u16), the 2 mp column nodes i (bytes 4.., u8; the dummy
+//               node n0max for the padding entry of an odd column)
+//   Dinv[S][32] f64    1 / D_k
+//   Lc[E2][32]  f64x2  column entries L_ik in pairs, steps consecutive
+struct URecLayout { long long desc, D, Lc, total; };
+__host__ __device__ __forceinline__ URecLayout urec_layout(int S, int E2) {
+  URecLayout U;
+  U.desc = 256;
+  U.D = a256(U.desc + 32ll * S);
+  U.Lc = U.D + 256ll * S;
+  U.total = a256(U.Lc + 512ll * E2);
+  return U;
+}
+constexpr int UMP = 13;  // largest pair count of a column (3D: <= 26 later neighbours)
+
+// One thread per warp slot.  fill = 0: check that the valid lanes of the warp share
+// one schedule (node of every step and column nodes; *bad = 1 otherwise) and size
+// the block; fill = 1: write it.  Empty slots get zero values (their vectors stay 0).
+__global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, int fill, int* bad) {
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((slot & ~31ll) >= nslots) return;  // warp-uniform
+  const long long w = slot >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long j = P.pord[slot];
+  int n = 0, nL = 0;
+  const char* rec = P.rec;
+  if (j >= 0) {
+    rec = P.rec + P.recoff[j * P.L];
+    const int4 h = *(const int4*)rec;
+    n = h.x; nL = h.z;
+  }
+  const bool valid = j >= 0 && n > 0;
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  const int ref = vm ? __ffs(vm) - 1 : 0;
+  const int S = vm ? __shfl_sync(0xffffffffu, n, ref) : 0;
+  const RecLayout R = rec_layout(n, nL);
+  const uint16_t* brp = (const uint16_t*)(rec + R.brp);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
+  const double* bLv = (const double*)(rec + R.bL);
+  const double* Dn = (const double*)(rec + R.D);
+  const URecLayout U = urec_layout(S, 0);
+  char* blk = fill ? P.trec + P.trecoff[w] : nullptr;
+  unsigned char* desc = fill ? (unsigned char*)(blk + U.desc) : nullptr;
+  double* Dd = fill ? (double*)(blk + U.D) : nullptr;
+  double* Lc = fill ? (double*)(blk + U.Lc) : nullptr;
+  bool mism = valid && n != S;
+  int kp = 0;
+  for (int t = 0; t < S; ++t) {
+    int node = 0, b0 = 0, cb = 0;
+    if (valid && t < n) { node = sch[t]; b0 = brp[t]; cb = brp[t + 1] - b0; }
+    const int rnode = __shfl_sync(0xffffffffu, node, ref), rcb = __shfl_sync(0xffffffffu, cb, ref);
+    if (valid && (node != rnode || cb != rcb)) mism = true;
+    const int mp = (rcb + 1) / 2;
+    if (mp > UMP) mism = true;
+    for (int k = 0; k < rcb && k < 2 * UMP; ++k) {
+      const int nd = (valid && k < cb) ? bkv[b0 + k] : 0;
+      const int rnd = __shfl_sync(0xffffffffu, nd, ref);
+      if (valid && nd != rnd) mism = true;
+      if (fill) {
+        if (lane == 0) desc[32 * t + 4 + k] = (unsigned char)rnd;
+        Lc[((long long)(kp + k / 2) * 32 + lane) * 2 + (k & 1)] = valid ? bLv[b0 + k] : 0.0;
+      }
+    }
+    if (fill) {
+      if (lane == 0) {
+        for (int k = rcb; k < 28; ++k) desc[32 * t + 4 + k] = (unsigned char)P.dummy;
+        *(uint32_t*)(desc + 32 * t) = (uint32_t)rnode | ((uint32_t)mp << 8) | ((uint32_t)kp << 16);
+      }
+      if (rcb & 1) Lc[((long long)(kp + rcb / 2) * 32 + lane) * 2 + 1] = 0.0;
+      Dd[t * 32 + lane] = valid ? 1.0 / Dn[node] : 0.0;
+    }
+    kp += mp;
+  }
+  if (kp > 65535) mism = true;
+  if (__any_sync(0xffffffffu, mism) && lane == 0) atomicExch(bad, 1);
+  if (!fill && lane == 0) P.sizes[w] = urec_layout(S, kp).total;
+  if (fill && lane == 0) *(int4*)blk = make_int4(S, kp, 0, 0);
+}
+
+// Slot order of U mode: the tile order, patches grouped by their level-0 box shape
+// (each group padded to whole warps).  *ok = 0 when some warp's patches do not share
+// one schedule (the caller falls back to T-records).
+static int urec_build(lorpc_prec* b, int TX, int TY, cudaStream_t s, int* ok) {
+  *ok = 0;
+  const std::vector<int> ord = tile_order(b, TX, TY);
+  const PatchGeom G = make_geom(b);
+  std::map<int, std::vector<int>> groups;
+  for (int j : ord) {
+    if (j < 0) continue;
+    int lo[3], ext[3];
+    patch_box(G, j, 0, lo, ext);
+    groups[ext[0] | (ext[1] << 10) | (ext[2] << 20)].push_back(j);
+  }
+  std::vector<int> uord;
+  uord.reserve(ord.size() + 32 * groups.size());
+  for (auto& g : groups) {
+    uord.insert(uord.end(), g.second.begin(), g.second.end());
+    uord.resize((uord.size() + 31) / 32 * 32, -1);
+  }
+  const long long nslots = (long long)uord.size(), nw = nslots / 32;
+  if (nslots == 0) return LORPC_OK;
+  LORPC_TRY(dalloc(&b->pord, uord.size()));
+  LORPC_CUDA(cudaMemcpyAsync(b->pord, uord.data(), sizeof(int) * uord.size(), cudaMemcpyHostToDevice, s));
+  TRecParams P{};
+  P.rec = b->rec; P.recoff = b->recoff; P.pord = b->pord; P.L = b->L; P.dummy = b->max_n[0];
+  long long* sizes = nullptr;
+  int* bad = nullptr;
+  LORPC_TRY(dalloc(&sizes, (size_t)nw));
+  LORPC_TRY(dalloc(&bad, 1));
+  LORPC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  P.sizes = sizes;
+  const unsigned blocks = (unsigned)((nslots + 127) / 128);
+  k_urec<<<blocks, 128, 0, s>>>(P, nslots, 0, bad);
+  LORPC_LAUNCHED();
+  std::vector<long long> h((size_t)nw);
+  int hbad = 0;
+  LORPC_CUDA(cudaMemcpyAsync(h.data(), sizes, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  if (hbad) {
+    dfree(sizes); dfree(bad); dfree(b->pord);
+    b->pord = nullptr;
+    return LORPC_OK;
+  }
+  long long off = 0;
+  for (auto& v : h) { const long long sz = v; v = off; off += sz; }
+  b->trec_bytes = off;
+  LORPC_TRY(dalloc(&b->trec, (size_t)off));
+  LORPC_TRY(dalloc(&b->trecoff, h.size()));
+  LORPC_CUDA(cudaMemcpyAsync(b->trecoff, h.data(), sizeof(long long) * h.size(), cudaMemcpyHostToDevice, s));
+  P.trec = b->trec; P.trecoff = b->trecoff;
+  k_urec<<<blocks, 128, 0, s>>>(P, nslots, 1, bad);
+  LORPC_LAUNCHED();
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  dfree(sizes); dfree(bad);
+  b->tslots = nslots;
+  *ok = 1;
+  return LORPC_OK;
+}
+
+static int tmode_finish(lorpc_prec* b, cudaStream_t s);
+
 int trec_build(lorpc_prec* b, cudaStream_t s) {
-  const long long nw = (b->J + 31) / 32, nslots = nw * 32;
   int TX = 32, TY = 32;  // measured on C5 (r01): 32 x 32 < 32 x 16 < 32 x 8 < lexicographic in V-cycle time
   if (const char* e = getenv("LORPC_TILE")) {  // "0": lexicographic order; "TXxTY" otherwise
     if (atoi(e) == 0) TX = TY = 1 << 30;
     else sscanf(e, "%dx%d", &TX, &TY);
   }
+  // structure-only orderings (natural, RCM): one sweep schedule per warp (U-records)
+  b->umode = false;
+  const char* ue = getenv("LORPC_UMODE");
+  if (b->desc.ordering != 0 && !b->erng && b->max_n[0] <= 254 && !(ue && atoi(ue) == 0)) {
+    int ok = 0;
+    LORPC_TRY(urec_build(b, TX, TY, s, &ok));
+    if (ok) { b->umode = true; return tmode_finish(b, s); }
+  }
+  const long long nw = (b->J + 31) / 32, nslots = nw * 32;
   const std::vector<int> ord = tile_order(b, TX, TY);
+  b->tslots = nslots;
   LORPC_TRY(dalloc(&b->pord, ord.size()));
   LORPC_CUDA(cudaMemcpyAsync(b->pord, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice, s));
   TRecParams P{};
@@ -247,7 +412,12 @@ int trec_build(lorpc_prec* b, cudaStream_t s) {
   LORPC_LAUNCHED();
   LORPC_CUDA(cudaStreamSynchronize(s));
   dfree(sizes);
-  // packed dense coarse operators; park buffers x, y, s
+  return tmode_finish(b, s);
+}
+
+// packed dense coarse operators and park buffers x, y, s for the tslots warp slots of pord
+static int tmode_finish(lorpc_prec* b, cudaStream_t s) {
+  const long long nslots = b->tslots;
   const PatchGeom G = make_geom(b);
   const int npk = b->m->d == 3 ? TCoarse<3>::NPK : TCoarse<2>::NPK;
   LORPC_TRY(dalloc(&b->Cdi, (size_t)(nslots * npk)));
@@ -488,6 +658,143 @@ __device__ __forceinline__ void tsmooth(const char* __restrict__ blk, double* X,
   tsweep<NP, false, IW>(blk, X, TPFD, lane);
   X[LORPC_XS * dummy] = 0.0;
   tsweep<NP, true, IW>(blk, X, TPFD, lane);
+}
+
+
+// ------------------------------------------------------------------ U-mode sweeps
+// The same push-forward / pull-backward sweeps as tsweep, over a U-record: step t's
+// descriptor (node, pair count, column nodes) is the same in every lane (uniform
+// loads, warp-uniform dispatch on the pair count, no divergence), only the values
+// differ per lane.  One step of software pipelining (the next step's values and the
+// descriptor two steps ahead are loaded while a step is applied); the value stream
+// is prefetched into L2 TPFD pair rows ahead.
+struct UDesc { uint32_t w[8]; };
+__device__ __forceinline__ void uload_desc(UDesc& d, const uint4* p) {
+  const uint4 a = __ldg(p), c = __ldg(p + 1);
+  d.w[0] = a.x; d.w[1] = a.y; d.w[2] = a.z; d.w[3] = a.w;
+  d.w[4] = c.x; d.w[5] = c.y; d.w[6] = c.z; d.w[7] = c.w;
+}
+__device__ __forceinline__ int unode(const UDesc& d) { return d.w[0] & 0xff; }
+__device__ __forceinline__ int ump(const UDesc& d) { return (d.w[0] >> 8) & 0xff; }
+__device__ __forceinline__ int ukp(const UDesc& d) { return (int)(d.w[0] >> 16); }
+__device__ __forceinline__ int unb(const UDesc& d, int m) { return (d.w[1 + (m >> 2)] >> (8 * (m & 3))) & 0xff; }
+
+struct UStage {
+  double2 l[UMP];
+  double dinv;
+};
+template <bool BWD>
+__device__ __forceinline__ void uload(UStage& g, const UDesc& d, const double2* __restrict__ Lp,
+                                      const double* __restrict__ Dd, int t) {
+  const int mp = ump(d), kp = ukp(d);
+#pragma unroll
+  for (int p = 0; p < UMP; ++p)
+    if (p < mp) g.l[p] = LORPC_RLD(Lp + (long long)(kp + p) * 32);
+  if (!BWD) g.dinv = LORPC_RLD(Dd + 32 * t);
+}
+template <int MP>
+__device__ __forceinline__ void ufwd(const UStage& g, const UDesc& d, double* X) {
+  const int k = unode(d);
+  const double yk = X[LORPC_XS * k];
+  double v[2 * MP + 1];
+#pragma unroll
+  for (int m = 0; m < 2 * MP; ++m) v[m] = X[LORPC_XS * unb(d, m)];
+#pragma unroll
+  for (int p = 0; p < MP; ++p) {
+    X[LORPC_XS * unb(d, 2 * p)] = v[2 * p] - g.l[p].x * yk;
+    X[LORPC_XS * unb(d, 2 * p + 1)] = v[2 * p + 1] - g.l[p].y * yk;
+  }
+  X[LORPC_XS * k] = yk * g.dinv;
+}
+template <int MP>
+__device__ __forceinline__ void ubwd(const UStage& g, const UDesc& d, double* X) {
+  const int k = unode(d);
+  double a[4] = {X[LORPC_XS * k], 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int p = 0; p < MP; ++p) {
+    a[2 * (p & 1)] -= g.l[p].x * X[LORPC_XS * unb(d, 2 * p)];
+    a[2 * (p & 1) + 1] -= g.l[p].y * X[LORPC_XS * unb(d, 2 * p + 1)];
+  }
+  X[LORPC_XS * k] = (a[0] + a[1]) + (a[2] + a[3]);
+}
+template <bool BWD, int MP>
+__device__ __forceinline__ void ustep_mp(const UStage& g, const UDesc& d, double* X) {
+  if (BWD) ubwd<MP>(g, d, X); else ufwd<MP>(g, d, X);
+}
+template <bool BWD>
+__device__ __forceinline__ void ustep(const UStage& g, const UDesc& d, double* X) {
+  switch (ump(d)) {  // warp-uniform
+    case 0: ustep_mp<BWD, 0>(g, d, X); break;
+    case 1: ustep_mp<BWD, 1>(g, d, X); break;
+    case 2: ustep_mp<BWD, 2>(g, d, X); break;
+    case 3: ustep_mp<BWD, 3>(g, d, X); break;
+    case 4: ustep_mp<BWD, 4>(g, d, X); break;
+    case 5: ustep_mp<BWD, 5>(g, d, X); break;
+    case 6: ustep_mp<BWD, 6>(g, d, X); break;
+    case 7: ustep_mp<BWD, 7>(g, d, X); break;
+    case 8: ustep_mp<BWD, 8>(g, d, X); break;
+    case 9: ustep_mp<BWD, 9>(g, d, X); break;
+    case 10: ustep_mp<BWD, 10>(g, d, X); break;
+    case 11: ustep_mp<BWD, 11>(g, d, X); break;
+    case 12: ustep_mp<BWD, 12>(g, d, X); break;
+    default: ustep_mp<BWD, 13>(g, d, X); break;
+  }
+}
+template <bool BWD>
+__device__ __forceinline__ void usweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
+  const int4 hd = __ldg((const int4*)blk);
+  const int S = hd.x, E2 = hd.y;
+  if (S == 0) return;
+  const URecLayout U = urec_layout(S, E2);
+  const uint4* Dsc = (const uint4*)(blk + U.desc);
+  const double* Dd = (const double*)(blk + U.D) + lane;
+  const double2* Lp = (const double2*)(blk + U.Lc) + lane;
+  if (lane == 0) {
+    l2_prefetch(Dsc, 32u * S);
+    if (!BWD) l2_prefetch(Dd - lane, 256u * S);
+  }
+  int pf = BWD ? E2 : 0;
+  auto st = [&](int q) { return BWD ? S - 1 - q : q; };
+  auto prefetch = [&](const UDesc& d) {
+    if (lane != 0) return;
+    if (!BWD) {
+      const int kp = ukp(d);
+      while (pf < E2 && pf < kp + TPFD) {
+        const int nr = min(LORPC_PFR, E2 - pf);
+        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
+        pf += nr;
+      }
+    } else {
+      const int kp = ukp(d) + ump(d);
+      while (pf > 0 && pf > kp - TPFD) {
+        const int nr = min(LORPC_PFR, pf);
+        pf -= nr;
+        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
+      }
+    }
+  };
+  UDesc dA, dB, dN;
+  UStage A, B;
+  uload_desc(dA, Dsc + 2 * st(0));
+  if (S > 1) uload_desc(dB, Dsc + 2 * st(1));
+  uload<BWD>(A, dA, Lp, Dd, st(0));
+  for (int q = 0; q < S; q += 2) {
+    prefetch(dA);
+    if (q + 1 < S) uload<BWD>(B, dB, Lp, Dd, st(q + 1));
+    if (q + 2 < S) uload_desc(dN, Dsc + 2 * st(q + 2));
+    ustep<BWD>(A, dA, X);
+    if (q + 1 >= S) break;
+    dA = dN;
+    if (q + 2 < S) uload<BWD>(A, dA, Lp, Dd, st(q + 2));
+    if (q + 3 < S) uload_desc(dN, Dsc + 2 * st(q + 3));
+    ustep<BWD>(B, dB, X);
+    dB = dN;
+  }
+}
+__device__ __forceinline__ void usmooth(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
+  usweep<false>(blk, X, TPFD, lane);
+  X[LORPC_XS * dummy] = 0.0;
+  usweep<true>(blk, X, TPFD, lane);
 }
 
 // ------------------------------------------------------------------ middle phase
@@ -844,13 +1151,15 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
 // ------------------------------------------------------------------ smoothing phases
 // pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
 // post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
+// IW = 0: U-records (one schedule per warp), else T-records with IW-byte node indices.
 template <int DIM, bool POST, int IW>
 __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   constexpr int NP = DIM == 3 ? 13 : 4;
   const int lane = threadIdx.x;
   const long long w = blockIdx.x;
   const int n0 = P.n0max;
-  const int nq = (int)min(32ll, P.J - w * 32);
+  const long long jl = P.pord[w * 32 + lane];
+  const bool valid = jl >= 0;
   const char* blk = P.trec + P.trecoff[w];
   const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
   // gather / scatter lane = patch: with the unpadded layout (stride LORPC_XS = 32)
@@ -858,8 +1167,8 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   // x-consecutive patches are p apart in r / z
   TPatch c{};
   float rex = 1.0f, rexy = 1.0f;
-  if (lane < nq) {
-    c = tpatch<DIM>(P.G, P.pord[w * 32 + lane]);
+  if (valid) {
+    c = tpatch<DIM>(P.G, jl);
     rex = 1.0f / c.ext[0]; rexy = 1.0f / (c.ext[0] * c.ext[1]);
   }
   auto gidx = [&](int i) {
@@ -870,19 +1179,20 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   const long long col = w * (long long)n0 * 32 + lane;
   if (!POST) {
     for (int i = 0; i < n0; ++i)  // r_j = I_j^T r (a5)
-      tsm[VO(i, lane)] = (lane < nq && i < c.n) ? __ldg(P.r + gidx(i)) : 0.0;
+      tsm[VO(i, lane)] = (valid && i < c.n) ? __ldg(P.r + gidx(i)) : 0.0;
   } else {
     for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] = __ldcs(P.spark + col + i * 32);
   }
   tsm[VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
-  tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
+  if constexpr (IW == 0) usmooth(blk, tsm + lane, n0, P.pfd, lane);
+  else tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
   __syncwarp();
   if (!POST) {
     for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[VO(i, lane)]);
   } else {
     for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] += __ldcs(P.ypark + col + i * 32);  // z_j = y + M^{-1} s
-    if (lane < nq)
+    if (valid)
       for (int i = 0; i < c.n; ++i) atomicAdd(P.z + gidx(i), tsm[VO(i, lane)]);  // z += I_j z_j (a8)
   }
 }
@@ -894,7 +1204,7 @@ static TcParams make_tparams(const lorpc_prec* b, const double* r, double* z) {
   P.W = b->wtab;
   memcpy(P.woff, b->woff[0], sizeof(P.woff));
   P.trec = b->trec; P.trecoff = b->trecoff; P.pord = b->pord;
-  P.J = b->J; P.nslots = (b->J + 31) / 32 * 32;
+  P.J = b->J; P.nslots = b->tslots;
   P.Cp = b->Cdi;
   P.n0max = b->max_n[0];
   const long long pcol = P.nslots * b->max_n[0];
@@ -940,7 +1250,10 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   }
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
   const unsigned wblocks = (unsigned)(P.nslots / 32), mblocks = (unsigned)((P.nslots + 127) / 128);
-  if (b->m->d == 2) {
+  if (b->umode) {
+    if (b->m->d == 2) LORPC_TRY((tlaunch<2, 0>(P, wblocks, mblocks, smem, s, false)));
+    else LORPC_TRY((tlaunch<3, 0>(P, wblocks, mblocks, smem, s, b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE"))));
+  } else if (b->m->d == 2) {
     if (tiw(P.n0max) == 1) LORPC_TRY((tlaunch<2, 1>(P, wblocks, mblocks, smem, s, false)));
     else LORPC_TRY((tlaunch<2, 2>(P, wblocks, mblocks, smem, s, false)));
   } else {

@@ -32,11 +32,11 @@ def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-def _cg(L, cfg):
+def _cg(L, cfg, ordering="mdf"):
     mesh = L.Mesh(cfg.dim, cfg.n, cfg.p, vertices(cfg))
-    prec = L.Prec(L.Lor(mesh), patch_kind=cfg.patch_kind)
+    prec = L.Prec(L.Lor(mesh), patch_kind=cfg.patch_kind, ordering=ordering)
     P = O.Problem.from_config(cfg)
-    P.schwarz_setup(cfg.patch_kind, "mdf", "gmg")
+    P.schwarz_setup(cfg.patch_kind, ordering, "gmg")
     return mesh, prec, P
 
 
@@ -50,12 +50,15 @@ def _pcg_check(L, mesh, prec, P, bo, tol):
     return rep, ro
 
 
-def test_c5_recipe_32cubed_multi_tile(L):
+@pytest.mark.parametrize("ordering", ["mdf", "rcm"])
+def test_c5_recipe_32cubed_multi_tile(L, ordering):
     """C5 recipe at 32^3 (33^3 vertex patches: two 32 x 32 warp-slot tiles per axis of
-    the thread-mode V-cycle): element-wise preconditioner parity and PCG."""
+    the thread-mode V-cycle; with RCM the U-record kernels, patches grouped into warps
+    by box shape): element-wise preconditioner parity and PCG."""
     cfg = small_config("C5", (32, 32, 32))
-    mesh, prec, P = _cg(L, cfg)
+    mesh, prec, P = _cg(L, cfg, ordering)
     assert "thread-mode" in prec.kernel()
+    assert ("U-records" in prec.kernel()) == (ordering == "rcm")
     r = parity_vector(P.ndof, seed=50)
     X = P.node_coords()
     free = np.all((X > 1e-12) & (X < 1 - 1e-12), axis=1)
@@ -114,8 +117,9 @@ def test_c4_recipe_16cubed_sipg(L, c):
 
 
 @pytest.mark.slow
-def test_c5_recipe_64cubed_pcg(L):
+@pytest.mark.parametrize("ordering", ["mdf", "rcm"])
+def test_c5_recipe_64cubed_pcg(L, ordering):
     """C5 recipe at 64^3 (7.2M DOFs), PCG against the oracle."""
     cfg = small_config("C5", (64, 64, 64))
-    mesh, prec, P = _cg(L, cfg)
+    mesh, prec, P = _cg(L, cfg, ordering)
     _pcg_check(L, mesh, prec, P, random_free_rhs(cfg), cfg.tol)
