@@ -4,8 +4,8 @@
 // Per element: gather the (p+1)^d tile (Dirichlet entries masked to 0) ->
 // 1D B/D contractions to the q^d Gauss points (q = p+1) -> multiply by the
 // symmetric G_q -> transposed contractions -> scatter-add (atomics; free
-// nodes only).  3D: one thread per (x,y) column of the tile, z contractions in
-// registers, x/y contractions through shared memory; several elements per CTA.
+// nodes only).  3D: one thread per line of the tile, every contraction in registers,
+// four transposes through shared memory (k_cg3); several elements per CTA.
 // y_D = x_D (symmetric Dirichlet elimination) is written by the pre-pass.
 #include "device.cuh"
 
@@ -24,42 +24,68 @@ __global__ void k_pre(const double* __restrict__ x, double* __restrict__ y, int3
   y[g] = d ? x[g] : 0.0;
 }
 
-// Q consecutive doubles from shared memory: 16-byte loads when Q is even (every read
-// below starts at a multiple of Q doubles of a 16-byte-aligned array)
+// Shared-memory layout of one transposed quantity of one element (row a2): Q^3 values
+// addressed a * SA + k * SK + b, element stride SE (doubles).  The strides are chosen
+// (offline bank model, scalar 64-bit accesses, lanes x-fastest over Q x Q x EB) so
+// that both the writer pattern (lanes (i, j) at i SA + k SK + j or j SA + k SK + i,
+// fixed k) and the reader pattern (lanes (i, j) at i SA + j SK + b or j SA + i SK + b,
+// fixed b) are free of bank conflicts for Q = 2, 4 and nearly so otherwise.
+template <int Q> struct CgLay;
+template <> struct CgLay<2> { static constexpr int SK = 3, SA = 6, SE = 12; };
+template <> struct CgLay<3> { static constexpr int SK = 3, SA = 9, SE = 27; };
+template <> struct CgLay<4> { static constexpr int SK = 5, SA = 20, SE = 80; };
+template <> struct CgLay<5> { static constexpr int SK = 5, SA = 29, SE = 149; };
+template <> struct CgLay<6> { static constexpr int SK = 7, SA = 42, SE = 252; };
+template <> struct CgLay<7> { static constexpr int SK = 9, SA = 63, SE = 441; };
+
+// one element's threads sync: its Q^2 threads lie in one warp when Q^2 divides 32
 template <int Q>
-__device__ __forceinline__ void lds_vec(const double* p, double (&v)[Q]) {
-  if constexpr (Q % 2 == 0) {
-#pragma unroll
-    for (int i = 0; i < Q / 2; ++i) {
-      const double2 t = reinterpret_cast<const double2*>(p)[i];
-      v[2 * i] = t.x;
-      v[2 * i + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < Q; ++i) v[i] = p[i];
-  }
+__device__ __forceinline__ void cg_sync() {
+  if constexpr (32 % (Q * Q) == 0) __syncwarp(); else __syncthreads();
 }
 
+// 256-bit read-only load of four consecutive doubles (32-byte aligned)
+__device__ __forceinline__ void ldg256(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+
+// 3D operator, line-per-thread sum factorisation.  Thread (i, j) of an element owns a
+// whole line of Q values in the direction being contracted, so every 1D contraction
+// runs in registers with the basis matrices read as constant-bank operands
+// (compile-time indices into the kernel parameter), and the data moves between the
+// three line orientations by four transposes through shared memory (each value is
+// written once and read once: 10 Q values per thread in, 10 Q out, against 22 Q
+// reads of the stage-per-direction form):
+//   z-lines at the nodes (a, b): u -> Bz u, Dz u                        [T1: -> y-lines]
+//   y-lines (a, qz): -> By Bz u, Dy Bz u, By Dz u                       [T2: -> x-lines]
+//   x-lines at the points (qy, qz): gradient, times G_q (one 256-bit load per
+//     component when Q = 4), transposed x contraction                   [T2^T]
+//   y-lines: transposed y contraction                                   [T1^T]
+//   z-lines: transposed z contraction, scatter-add (atomics; free nodes only).
 template <int P, int EB>
 __global__ void __launch_bounds__((P + 1) * (P + 1) * EB)
 k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ G, int3 n, int3 N,
-      Basis1D bs, long long e0, long long e1) {
+      const __grid_constant__ Basis1D bs, long long e0, long long e1) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q * Q * Q;
-  __shared__ double sB[Q2], sD[Q2];
-  // stage layouts: every contraction reads its Q operands contiguously (lds_vec)
-  __shared__ __align__(16) double S[EB][3][Q3];
-  const int tx = threadIdx.x, ty = threadIdx.y, te = threadIdx.z;
-  const int lt = tx + Q * (ty + Q * te);
-  for (int i = lt; i < Q2; i += Q2 * EB) { sB[i] = bs.B[i]; sD[i] = bs.D[i]; }
+  constexpr int SK = CgLay<Q>::SK, SA = CgLay<Q>::SA, SE = CgLay<Q>::SE;
+  __shared__ double S[2][3][EB * SE];
+  const int ti = threadIdx.x, tj = threadIdx.y, te = threadIdx.z;
   const long long e = e0 + (long long)blockIdx.x * EB + te;  // elements [e0, e1) (slab layers)
   const bool active = e < e1;
   int ex = 0, ey = 0, ez = 0;
   if (active) { ex = (int)(e % n.x); ey = (int)((e / n.x) % n.y); ez = (int)(e / ((long long)n.x * n.y)); }
-  const int gx = ex * P + tx, gy = ey * P + ty;
+  const int gx = ex * P + ti, gy = ey * P + tj;
   const bool bxy = gx == 0 || gx == N.x - 1 || gy == 0 || gy == N.y - 1;
   const long long base = gx + (long long)N.x * gy;
   const long long sz = (long long)N.x * N.y;
+  // form-1 addresses (writer i SA + k SK + j, reader i SA + j SK + b), form 2 with i, j swapped
+  double* const A0 = &S[0][0][te * SE];
+  double* const B0 = &S[1][0][te * SE];
+  constexpr int SQ = EB * SE;  // quantity stride
+  const int w1 = ti * SA + tj, r1 = ti * SA + tj * SK;
+  const int w2 = tj * SA + ti, r2 = tj * SA + ti * SK;
+
+  // z-lines at the nodes (a = ti, b = tj)
   double u[Q];
 #pragma unroll
   for (int c = 0; c < Q; ++c) {
@@ -67,103 +93,90 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
     const bool dir = bxy || gz == 0 || gz == N.z - 1;
     u[c] = (active && !dir) ? x[base + sz * gz] : 0.0;
   }
-  __syncthreads();
-  double* S0 = S[te][0];
-  double* S1 = S[te][1];
-  double* S2 = S[te][2];
-  // z contraction (registers)
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double bu = 0.0, du = 0.0;
 #pragma unroll
-    for (int c = 0; c < Q; ++c) { bu += sB[qz * Q + c] * u[c]; du += sD[qz * Q + c] * u[c]; }
-    S0[qz * Q2 + tx * Q + ty] = bu;  // [qz][a][b]
-    S1[qz * Q2 + tx * Q + ty] = du;
+    for (int c = 0; c < Q; ++c) { bu += bs.B[qz * Q + c] * u[c]; du += bs.D[qz * Q + c] * u[c]; }
+    A0[w1 + qz * SK] = bu;
+    A0[SQ + w1 + qz * SK] = du;
   }
-  __syncthreads();
-  // y contraction: thread (a = tx, qy = ty)
-  double r1[Q], r2[Q], r3[Q];
+  cg_sync<Q>();
+  // y-lines (a = ti, qz = tj)
+  double v0[Q], v1[Q], v2[Q];
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    double t1 = 0.0, t2 = 0.0, t3 = 0.0, v0[Q], v1[Q];
-    lds_vec<Q>(S0 + qz * Q2 + tx * Q, v0);
-    lds_vec<Q>(S1 + qz * Q2 + tx * Q, v1);
+  for (int b = 0; b < Q; ++b) { v0[b] = A0[r1 + b]; v1[b] = A0[SQ + r1 + b]; }
+#pragma unroll
+  for (int qy = 0; qy < Q; ++qy) {
+    double bb = 0.0, db = 0.0, bd = 0.0;
 #pragma unroll
     for (int b = 0; b < Q; ++b) {
-      t1 += sB[ty * Q + b] * v0[b]; t2 += sD[ty * Q + b] * v0[b]; t3 += sB[ty * Q + b] * v1[b];
+      bb += bs.B[qy * Q + b] * v0[b]; db += bs.D[qy * Q + b] * v0[b]; bd += bs.B[qy * Q + b] * v1[b];
     }
-    r1[qz] = t1; r2[qz] = t2; r3[qz] = t3;
+    B0[w2 + qy * SK] = bb;           // By Bz u  (-> Dx: d/dx)
+    B0[SQ + w2 + qy * SK] = db;      // Dy Bz u  (-> Bx: d/dy)
+    B0[2 * SQ + w2 + qy * SK] = bd;  // By Dz u  (-> Bx: d/dz)
   }
-  __syncthreads();
+  cg_sync<Q>();
+  // x-lines at the quadrature points (qy = ti, qz = tj)
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    S0[qz * Q2 + ty * Q + tx] = r1[qz]; S1[qz * Q2 + ty * Q + tx] = r2[qz]; S2[qz * Q2 + ty * Q + tx] = r3[qz];
-  }
-  __syncthreads();
-  // x contraction + geometric factors: thread (qx = tx, qy = ty)
-  const double* Ge = G + (active ? e : 0) * 6 * Q3;
+  for (int a = 0; a < Q; ++a) { v0[a] = B0[r2 + a]; v1[a] = B0[SQ + r2 + a]; v2[a] = B0[2 * SQ + r2 + a]; }
+  double f0[Q], f1[Q], f2[Q];
+  {
+    const double* Ge = G + (active ? e : 0) * 6 * Q3 + Q * (ti + Q * tj);
+    double g[6][Q];
+    if constexpr (Q == 4) {
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    double gxv = 0.0, gyv = 0.0, gzv = 0.0, v0[Q], v1[Q], v2[Q];
-    lds_vec<Q>(S0 + qz * Q2 + ty * Q, v0);
-    lds_vec<Q>(S1 + qz * Q2 + ty * Q, v1);
-    lds_vec<Q>(S2 + qz * Q2 + ty * Q, v2);
+      for (int c = 0; c < 6; ++c) ldg256(Ge + c * Q3, g[c]);
+    } else {
 #pragma unroll
-    for (int a = 0; a < Q; ++a) {
-      gxv += sD[tx * Q + a] * v0[a];
-      gyv += sB[tx * Q + a] * v1[a];
-      gzv += sB[tx * Q + a] * v2[a];
+      for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) g[c][qx] = __ldg(Ge + c * Q3 + qx);
     }
-    const int iq = tx + Q * (ty + Q * qz);
-    const double g00 = Ge[0 * Q3 + iq], g01 = Ge[1 * Q3 + iq], g02 = Ge[2 * Q3 + iq];
-    const double g11 = Ge[3 * Q3 + iq], g12 = Ge[4 * Q3 + iq], g22 = Ge[5 * Q3 + iq];
-    r1[qz] = g00 * gxv + g01 * gyv + g02 * gzv;
-    r2[qz] = g01 * gxv + g11 * gyv + g12 * gzv;
-    r3[qz] = g02 * gxv + g12 * gyv + g22 * gzv;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    S0[qz * Q2 + ty * Q + tx] = r1[qz]; S1[qz * Q2 + ty * Q + tx] = r2[qz]; S2[qz * Q2 + ty * Q + tx] = r3[qz];
-  }
-  __syncthreads();
-  // x^T: thread (a = tx, qy = ty)
-#pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    double w1 = 0.0, w2 = 0.0, w3 = 0.0, v0[Q], v1[Q], v2[Q];
-    lds_vec<Q>(S0 + qz * Q2 + ty * Q, v0);
-    lds_vec<Q>(S1 + qz * Q2 + ty * Q, v1);
-    lds_vec<Q>(S2 + qz * Q2 + ty * Q, v2);
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
-      w1 += sD[qx * Q + tx] * v0[qx];
-      w2 += sB[qx * Q + tx] * v1[qx];
-      w3 += sB[qx * Q + tx] * v2[qx];
+      double gxv = 0.0, gyv = 0.0, gzv = 0.0;
+#pragma unroll
+      for (int a = 0; a < Q; ++a) {
+        gxv += bs.D[qx * Q + a] * v0[a]; gyv += bs.B[qx * Q + a] * v1[a]; gzv += bs.B[qx * Q + a] * v2[a];
+      }
+      f0[qx] = g[0][qx] * gxv + g[1][qx] * gyv + g[2][qx] * gzv;
+      f1[qx] = g[1][qx] * gxv + g[3][qx] * gyv + g[4][qx] * gzv;
+      f2[qx] = g[2][qx] * gxv + g[4][qx] * gyv + g[5][qx] * gzv;
     }
-    r1[qz] = w1; r2[qz] = w2; r3[qz] = w3;
   }
-  __syncthreads();
+  // transposed x contraction (same lines), then to y-lines
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {  // [qz][a][qy]
-    S0[qz * Q2 + tx * Q + ty] = r1[qz]; S1[qz * Q2 + tx * Q + ty] = r2[qz]; S2[qz * Q2 + tx * Q + ty] = r3[qz];
+  for (int a = 0; a < Q; ++a) {
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      p0 += bs.D[qx * Q + a] * f0[qx]; p1 += bs.B[qx * Q + a] * f1[qx]; p2 += bs.B[qx * Q + a] * f2[qx];
+    }
+    A0[w2 + a * SK] = p0;
+    A0[SQ + w2 + a * SK] = p1;
+    A0[2 * SQ + w2 + a * SK] = p2;
   }
-  __syncthreads();
-  // y^T: thread (a = tx, b = ty) -> YB (then B_z^T), YD (then D_z^T)
-  double yb[Q], yd[Q];
+  cg_sync<Q>();
+  // y-lines (a = ti, qz = tj): transposed y contraction
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) {
-    double t1 = 0.0, t2 = 0.0, v0[Q], v1[Q], v2[Q];
-    lds_vec<Q>(S0 + qz * Q2 + tx * Q, v0);
-    lds_vec<Q>(S1 + qz * Q2 + tx * Q, v1);
-    lds_vec<Q>(S2 + qz * Q2 + tx * Q, v2);
+  for (int qy = 0; qy < Q; ++qy) { v0[qy] = A0[r2 + qy]; v1[qy] = A0[SQ + r2 + qy]; v2[qy] = A0[2 * SQ + r2 + qy]; }
+#pragma unroll
+  for (int b = 0; b < Q; ++b) {
+    double t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
-      t1 += sB[qy * Q + ty] * v0[qy] + sD[qy * Q + ty] * v1[qy];
-      t2 += sB[qy * Q + ty] * v2[qy];
+      t1 += bs.B[qy * Q + b] * v0[qy] + bs.D[qy * Q + b] * v1[qy];
+      t2 += bs.B[qy * Q + b] * v2[qy];
     }
-    yb[qz] = t1; yd[qz] = t2;
+    B0[w1 + b * SK] = t1;       // (-> Bz^T)
+    B0[SQ + w1 + b * SK] = t2;  // (-> Dz^T)
   }
-  // z^T and scatter
+  cg_sync<Q>();
+  // z-lines at the nodes (a = ti, b = tj): transposed z contraction and scatter
+#pragma unroll
+  for (int qz = 0; qz < Q; ++qz) { v0[qz] = B0[r1 + qz]; v1[qz] = B0[SQ + r1 + qz]; }
   if (!active || bxy) return;
 #pragma unroll
   for (int c = 0; c < Q; ++c) {
@@ -171,7 +184,7 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
     if (gz == 0 || gz == N.z - 1) continue;
     double v = 0.0;
 #pragma unroll
-    for (int qz = 0; qz < Q; ++qz) v += sB[qz * Q + c] * yb[qz] + sD[qz * Q + c] * yd[qz];
+    for (int qz = 0; qz < Q; ++qz) v += bs.B[qz * Q + c] * v0[qz] + bs.D[qz * Q + c] * v1[qz];
     atomicAdd(y + base + sz * gz, v);
   }
 }
@@ -233,7 +246,7 @@ k_cg2(const double* __restrict__ x, double* __restrict__ y, const double* __rest
 template <int P>
 static void launch3(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
   constexpr int Q = P + 1;
-  constexpr int EB = (Q * Q <= 16) ? 8 : (Q * Q <= 36 ? 4 : 2);
+  constexpr int EB = (Q * Q <= 16) ? 8 : (Q * Q <= 25 ? 4 : 2);  // 6 EB SE doubles of shared memory <= 48 KB
   int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
   dim3 blk(Q, Q, EB);
