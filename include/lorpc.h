@@ -167,7 +167,9 @@ int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels);
  * memory), 1 = thread mode (vcycle_t.cu: one lane per patch, warp-interleaved
  * factors), 2 = W mode (vcycle_w.cu: warp-per-patch fused V-cycle, opt-in through
  * LORPC_WMODE=1), 3 = thread mode with U-records (structure-only orderings: natural,
- * RCM; the warp's patches share one sweep schedule, only factor values per lane).
+ * RCM; the warp's patches share one sweep schedule, only factor values per lane),
+ * 4 = Q mode (vcycle_w.cu: fused V-cycle with 2 / 4 / 8 lanes per patch, one sweep
+ * schedule per warp, factors streamed through a cp.async ring; LORPC_QMODE=1).
  * Errors: LORPC_ERR_ARG on NULL. */
 int lorpc_prec_kernel(const lorpc_prec* b, int* mode);
 /* Algorithmic byte-model inputs: factor_values = sum over

@@ -209,6 +209,7 @@ void lorpc_prec_destroy(lorpc_prec* b) {
   if (!b) return;
   dfree(b->rec); dfree(b->recoff); dfree(b->trec); dfree(b->trecoff); dfree(b->zpark); dfree(b->Cdi); dfree(b->pord);
   dfree(b->wrec); dfree(b->wrecoff); dfree(b->Cq); dfree(b->erng);
+  dfree(b->qrec); dfree(b->qrecoff); dfree(b->qsched);
   for (int l = 0; l < MAXL; ++l) { dfree(b->sgr[l]); dfree(b->sgz[l]); dfree(b->sgl[l]); dfree(b->sgw[l]); }
   for (int i = 0; i < MAXC; ++i) {
     if (i > 0) dfree(b->Ac[i]);
@@ -246,7 +247,7 @@ int lorpc_prec_info(const lorpc_prec* b, long long* n_patches, int* n_levels) {
 
 int lorpc_prec_kernel(const lorpc_prec* b, int* mode) {
   if (!b || !mode) return fail(LORPC_ERR_ARG, "prec_kernel: NULL");
-  *mode = b->wmode ? 2 : b->umode ? 3 : b->tmode ? 1 : 0;
+  *mode = b->qmode ? 4 : b->wmode ? 2 : b->umode ? 3 : b->tmode ? 1 : 0;
   return LORPC_OK;
 }
 

@@ -145,6 +145,14 @@ struct lorpc_prec {
   long long wslots = 0;
   double* Cq = nullptr;             // [wslots][378] packed dense coarse operators
   int wlp = 16;                     // lanes per patch of the W kernel (16: two patches per warp)
+  // Q mode (vcycle_w.cu): fused V-cycle, LP lanes per patch, factors streamed through a cp.async ring
+  bool qmode = false;
+  int qlp = 4, qcm = 2;             // lanes per patch; ring rows (pairs per lane) per sweep step
+  char* qrec = nullptr;             // per warp: {shape, S, E} | dinv[S][NPW] | values [E NPW] f64x2
+  long long* qrecoff = nullptr;     // [warps] byte offsets
+  long long qrec_bytes = 0;
+  char* qsched = nullptr;           // per box shape: the shared sweep schedule (header + node offsets)
+  int qsched_stride = 0;
   // single patch B(1) (single.cu): level-grid vectors r, z, s, w
   double* sgr[lorpc::MAXL] = {};
   double* sgz[lorpc::MAXL] = {};

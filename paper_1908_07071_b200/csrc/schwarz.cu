@@ -35,6 +35,8 @@ size_t tmode_smem(const lorpc_prec* b);
 int wrec_build(lorpc_prec* b, cudaStream_t s);          // vcycle_w.cu
 int single_setup(lorpc_prec* b);                        // single.cu
 size_t wmode_smem(const lorpc_prec* b);
+int qrec_build(lorpc_prec* b, cudaStream_t s, int* ok);  // vcycle_w.cu (Q mode)
+size_t qmode_smem(const lorpc_prec* b);
 
 // ------------------------------------------------------------------ MDF + ILU(0)
 __device__ __forceinline__ double q30(double x) {
@@ -671,6 +673,18 @@ int schwarz_build(lorpc_prec* b, cudaStream_t s) {
       LORPC_TRY(wrec_build(b, s));
       if (wmode_smem(b) > 227 * 1024) return fail(LORPC_ERR_SIZE, "wmode: record does not fit in shared memory");
       return LORPC_OK;
+    }
+    // Q mode (LP lanes per patch, factors streamed through a cp.async ring): structure-only
+    // orderings (natural, RCM) on the same patches; LORPC_QMODE=0 disables it
+    const char* eq = getenv("LORPC_QMODE");
+    if (eligible && b->desc.ordering != 0 && eq && atoi(eq) != 0) {
+      int ok = 0;
+      LORPC_TRY(qrec_build(b, s, &ok));
+      if (ok && qmode_smem(b) <= 227 * 1024) {
+        b->qmode = true;
+        return LORPC_OK;
+      }
+      if (ok) return fail(LORPC_ERR_SIZE, "qmode: shared memory");
     }
   }
   // thread-per-patch V-cycle when the warp's 32 patch vectors fit in shared memory

@@ -650,6 +650,7 @@ static int launch_vc(const VcParams& P, long long J, cudaStream_t s) {
 
 int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);  // vcycle_t.cu
 int vcycle_w_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);  // vcycle_w.cu
+int vcycle_q_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s);  // vcycle_w.cu
 
 int dense_coarse_setup(lorpc_prec* b, cudaStream_t s) {
   VcParams P = make_params(b, nullptr, nullptr);
@@ -659,6 +660,7 @@ int dense_coarse_setup(lorpc_prec* b, cudaStream_t s) {
 // z = sum_j I_j B_j I_j^T r over the patches (no coarse term, z not zeroed at Dirichlet nodes)
 int schwarz_apply_patches(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
   LORPC_CUDA(cudaMemsetAsync(z, 0, sizeof(double) * b->m->ndof_cg, s));
+  if (b->qmode) return vcycle_q_apply(b, r, z, s);
   if (b->wmode) return vcycle_w_apply(b, r, z, s);
   if (b->tmode) return vcycle_t_apply(b, r, z, s);
   VcParams P = make_params(b, r, z);
@@ -692,7 +694,8 @@ int schwarz_apply_cg(const lorpc_prec* b, const double* r, double* z, cudaStream
   lorpc_prec* bm = const_cast<lorpc_prec*>(b);
   const bool prof = bm->prof_on && bm->prof_n < (int)bm->prof_ev.size() / 2;
   if (prof) LORPC_CUDA(cudaEventRecord(bm->prof_ev[2 * bm->prof_n], s));
-  const int rc = b->wmode ? vcycle_w_apply(b, r, z, s)
+  const int rc = b->qmode ? vcycle_q_apply(b, r, z, s)
+                 : b->wmode ? vcycle_w_apply(b, r, z, s)
                  : b->tmode ? vcycle_t_apply(b, r, z, s)
                  : d == 2 ? launch_vc<2, false>(P, b->J, s) : launch_vc<3, false>(P, b->J, s);
   if (rc != LORPC_OK) return rc;

@@ -422,59 +422,13 @@ __device__ __forceinline__ void wres_lines(const WParams& P, const WBox& c, cons
   }
 }
 
-// LP = 16: two patches per warp, half-warp h = lane / 16 owns slot 2 blockIdx + h;
-// LP = 32: one patch per warp.
+// The coarse correction between the two smoothing steps, LP lanes per patch (lane hl
+// of the patch): s = r_j - A x (x-restricted on the fly), r_1 = P^T s, z_1 = C r_1,
+// X <- y = x + P z_1, S <- s = r_j - A y.  S doubles as the transfer scratch.
 template <int LP>
-__global__ void __launch_bounds__(32, LP == 32 ? 12 : 7) k_vw(WParams P) {
-  constexpr int PPW = 32 / LP;
-  const int lane = threadIdx.x, h = lane / LP, hl = lane & (LP - 1);
-  const long long slot = PPW * (long long)blockIdx.x + h;
-  const bool act = slot < P.nslots;
-  char* rs = (char*)(wsm + h * P.half_doubles);
-  double* X = (double*)(rs + P.rec_bytes);
-  double* S = X + P.vec_doubles;
-  // stage the record (one HBM pass; every later use of the factor reads shared memory)
-  if (act) {
-    const long long o0 = P.wrecoff[slot], o1 = P.wrecoff[slot + 1];
-    const int4* src = (const int4*)(P.wrec + o0);
-    int4* dst = (int4*)rs;
-    const int n16 = (int)((o1 - o0) >> 4);
-    for (int u = hl; u < n16; u += LP) dst[u] = __ldcs(src + u);
-  } else if (hl < 5) {
-    // empty slot: a valid empty record (header, round offsets and dummy entry all 0)
-    ((int4*)rs)[hl] = make_int4(0, 0, 0, 0);
-  }
-  WBox c;
-  c.n = 0;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) { c.lo[k] = 0; c.ext[k] = 0; c.cext[k] = 0; c.ec[k] = 1; }
-  if (act) {
-    const long long j = P.pord[slot];
-    int elo[3], ehi[3];
-    patch_elems(P.G, j, elo, ehi);
-    c.n = 1;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      c.ec[k] = ehi[k] - elo[k] + 1;
-      c.lo[k] = elo[k] * (P.G.ml[0] - 1) + 1;
-      c.ext[k] = c.ec[k] * (P.G.ml[0] - 1) - 1;
-      c.cext[k] = c.ec[k] * (P.G.ml[1] - 1) - 1;
-      c.n *= c.ext[k];
-    }
-  }
+__device__ __forceinline__ void wmid(const WParams& P, const WBox& c, double* X, double* S, bool act, long long slot,
+                                     int hl) {
   const int ex = c.ext[0], ey = c.ext[1];
-  const size_t Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-  const float rex = 1.0f / max(ex, 1), rexy = 1.0f / max(ex * ey, 1);
-  auto gidx = [&](int i) {
-    int ix, iy, iz;
-    box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
-    return (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (size_t)(c.lo[2] + iz));
-  };
-  for (int i = hl; i < c.n; i += LP) X[i] = __ldg(P.r + gidx(i));  // r_j = I_j^T r (a5)
-  if (hl == 0) { X[c.n] = 0.0; S[c.n] = 0.0; }                      // dummy node of the sweeps
-  __syncwarp();
-  wsmooth<LP>(rs, X, hl);                                                // x = M^{-1} r_j
-  __syncwarp();
   const double* Wx = P.W + P.woff[c.ec[0]];
   const double* Wy = P.W + P.woff[c.ec[1]];
   const double* Wz = P.W + P.woff[c.ec[2]];
@@ -540,6 +494,62 @@ __global__ void __launch_bounds__(32, LP == 32 ? 12 : 7) k_vw(WParams P) {
   }
   __syncwarp();
   wres_lines<LP, false>(P, c, X, S, Wx, hl);                             // s = r_j - A y
+}
+
+// LP = 16: two patches per warp, half-warp h = lane / 16 owns slot 2 blockIdx + h;
+// LP = 32: one patch per warp.
+template <int LP>
+__global__ void __launch_bounds__(32, LP == 32 ? 12 : 7) k_vw(WParams P) {
+  constexpr int PPW = 32 / LP;
+  const int lane = threadIdx.x, h = lane / LP, hl = lane & (LP - 1);
+  const long long slot = PPW * (long long)blockIdx.x + h;
+  const bool act = slot < P.nslots;
+  char* rs = (char*)(wsm + h * P.half_doubles);
+  double* X = (double*)(rs + P.rec_bytes);
+  double* S = X + P.vec_doubles;
+  // stage the record (one HBM pass; every later use of the factor reads shared memory)
+  if (act) {
+    const long long o0 = P.wrecoff[slot], o1 = P.wrecoff[slot + 1];
+    const int4* src = (const int4*)(P.wrec + o0);
+    int4* dst = (int4*)rs;
+    const int n16 = (int)((o1 - o0) >> 4);
+    for (int u = hl; u < n16; u += LP) dst[u] = __ldcs(src + u);
+  } else if (hl < 5) {
+    // empty slot: a valid empty record (header, round offsets and dummy entry all 0)
+    ((int4*)rs)[hl] = make_int4(0, 0, 0, 0);
+  }
+  WBox c;
+  c.n = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { c.lo[k] = 0; c.ext[k] = 0; c.cext[k] = 0; c.ec[k] = 1; }
+  if (act) {
+    const long long j = P.pord[slot];
+    int elo[3], ehi[3];
+    patch_elems(P.G, j, elo, ehi);
+    c.n = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      c.ec[k] = ehi[k] - elo[k] + 1;
+      c.lo[k] = elo[k] * (P.G.ml[0] - 1) + 1;
+      c.ext[k] = c.ec[k] * (P.G.ml[0] - 1) - 1;
+      c.cext[k] = c.ec[k] * (P.G.ml[1] - 1) - 1;
+      c.n *= c.ext[k];
+    }
+  }
+  const int ex = c.ext[0], ey = c.ext[1];
+  const size_t Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
+  const float rex = 1.0f / max(ex, 1), rexy = 1.0f / max(ex * ey, 1);
+  auto gidx = [&](int i) {
+    int ix, iy, iz;
+    box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
+    return (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (size_t)(c.lo[2] + iz));
+  };
+  for (int i = hl; i < c.n; i += LP) X[i] = __ldg(P.r + gidx(i));  // r_j = I_j^T r (a5)
+  if (hl == 0) { X[c.n] = 0.0; S[c.n] = 0.0; }                      // dummy node of the sweeps
+  __syncwarp();
+  wsmooth<LP>(rs, X, hl);                                                // x = M^{-1} r_j
+  __syncwarp();
+  wmid<LP>(P, c, X, S, act, slot, hl);
   if (hl == 0) S[c.n] = 0.0;
   __syncwarp();
   wsmooth<LP>(rs, S, hl);                                                // M^{-1} s
@@ -666,6 +676,526 @@ int vcycle_w_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   const WParams P = make_wparams(b, r, z);
   if (P.nslots == 0) return LORPC_OK;
   return b->wlp == 32 ? launch_vw<32>(P, s) : launch_vw<16>(P, s);
+}
+
+// ================================================================== Q mode
+// Fused V-cycle with LP lanes per patch (LP = 2, 4, 8; NPW = 32 / LP patches per warp)
+// for structure-only orderings (natural, RCM = reading r5): the patches of a warp have
+// the same free-node box, hence ONE sweep schedule (as the U-records of vcycle_t.cu).
+//
+// Why: the thread-per-patch kernels keep 224 patches per SM in flight (358 MB of
+// factors, nothing survives in the 126 MB L2 between the four sweeps, 4 x 23 GB per
+// apply on C5) and each lane's sweep is one long chain of dependent loads; the
+// warp-per-patch W mode reads the factor once but fits only ~14 patches per SM.
+// Q mode sits between: ~80 patches per SM (2 KB of vectors each; their factors,
+// ~0.9 MB per SM, mostly stay in L2 from one sweep to the next), the factor is never
+// staged whole but streams through a small cp.async ring (QD sweep steps ahead, no
+// registers held by loads in flight), and the LP lanes of a patch split each column.
+//
+// Sweeps: column steps as in the U-records.  Step t eliminates node k(t); its column
+// holds the entries L_ik of the later neighbours i, in pairs; lane hl of the patch
+// owns the pairs p = hl, hl + LP, ... (at most CM per step).  Forward (push): y_i -=
+// L_ik y_k for the lane's pairs, lane 0 stores x_k = y_k / D_k.  Backward (pull, steps
+// descending): the lanes' partial sums of L_ik x_i meet in a shuffle reduction.  One
+// __syncwarp per step.  Pairs past the column's end read zero-filled ring entries and
+// the dummy node n (value 0), so a step has no branches.
+//
+// Per box shape (device table, shared by all warps of that shape):
+//   int4 {S, E, mpmax, n}   steps, pairs per patch, widest column (pairs), nodes
+//   hdr[S]          u32   node k (bits 0-7) | pairs mp (8-15) | pairs before step t (16-31)
+//   idx[S][LP][CM]  u32   byte offsets 8 i0 | 8 i1 << 16 of the two nodes of pair hl + LP c
+// Per warp (Q-record, 256-byte aligned):
+//   int4 {shape, S, E, 0} | dinv[S][NPW] f64 | val[E NPW] f64x2: step t at pair offset
+//   kp(t) NPW, then patch q at q mp(t), pairs consecutive (no padding between steps)
+constexpr int QD = 4;  // sweep steps in flight in the cp.async ring
+
+__host__ __device__ __forceinline__ int qsched_bytes(int S, int LP, int CM) { return 16 + 4 * S + 4 * S * LP * CM; }
+__host__ __device__ __forceinline__ long long qrec_bytes(int S, long long E, int NPW) {
+  return (16 + 8ll * S * NPW + 16ll * E * NPW + 255) & ~255ll;
+}
+
+struct QBuildParams {
+  const char* rec;
+  const long long* recoff;
+  const int* pord;       // [nslots] patch of each slot (-1: empty)
+  const int* shape_ref;  // [nshapes] reference patch of each shape
+  const int* wshape;     // [warps] shape of each warp
+  int L, LP, CM, nshapes;
+  long long nslots;
+  int4* info;            // [nshapes] {S, E, mpmax, n}
+  char* sched;
+  int sched_stride;
+  char* qrec;
+  const long long* qrecoff;
+  int* bad;
+};
+
+// One thread per shape.  fill = 0: {S, E, mpmax, n} from the reference patch's record;
+// fill = 1: the schedule table.
+__global__ void k_qsched(QBuildParams P, int fill) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.nshapes) return;
+  const long long j = P.shape_ref[g];
+  const char* rec = P.rec + P.recoff[j * P.L];
+  const int4 h = *(const int4*)rec;
+  const int n = h.x, nL = h.z;
+  const RecLayout R = rec_layout(n, nL);
+  const uint16_t* brp = (const uint16_t*)(rec + R.brp);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
+  char* tab = P.sched + (size_t)g * P.sched_stride;
+  uint32_t* hdr = (uint32_t*)(tab + 16);
+  uint32_t* idx = hdr + n;
+  int kp = 0, mpmax = 0;
+  for (int t = 0; t < n; ++t) {
+    const int b0 = brp[t], cb = brp[t + 1] - b0, mp = (cb + 1) / 2;
+    mpmax = max(mpmax, mp);
+    if (fill) {
+      hdr[t] = (uint32_t)sch[t] | ((uint32_t)mp << 8) | ((uint32_t)kp << 16);
+      for (int hl = 0; hl < P.LP; ++hl)
+        for (int c = 0; c < P.CM; ++c) {
+          const int pr = hl + P.LP * c;
+          const int i0 = 2 * pr < cb ? bkv[b0 + 2 * pr] : n, i1 = 2 * pr + 1 < cb ? bkv[b0 + 2 * pr + 1] : n;
+          idx[(t * P.LP + hl) * P.CM + c] = (uint32_t)(8 * i0) | ((uint32_t)(8 * i1) << 16);
+        }
+    }
+    kp += mp;
+  }
+  if (!fill) P.info[g] = make_int4(n, kp, mpmax, n);
+  else *(int4*)tab = make_int4(n, kp, mpmax, n);
+}
+
+// One thread per patch slot: checks the patch against its shape's schedule (*bad = 1
+// on any difference) and writes its dinv and values into the warp's Q-record.
+__global__ void __launch_bounds__(128) k_qrec(QBuildParams P) {
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (slot >= P.nslots) return;
+  const int NPW = 32 / P.LP;
+  const long long w = slot / NPW;
+  const int q = (int)(slot % NPW);
+  const int g = P.wshape[w];
+  const char* tab = P.sched + (size_t)g * P.sched_stride;
+  const int4 ti = *(const int4*)tab;
+  const int S = ti.x, E = ti.y;
+  const uint32_t* hdr = (const uint32_t*)(tab + 16);
+  const uint32_t* idx = hdr + S;
+  char* blk = P.qrec + P.qrecoff[w];
+  if (q == 0) *(int4*)blk = make_int4(g, S, E, 0);
+  double* dv = (double*)(blk + 16);
+  double2* val = (double2*)(blk + 16 + 8ll * S * NPW);
+  const long long j = P.pord[slot];
+  if (j < 0) {  // empty slot: zero factor (its vectors stay zero)
+    for (int t = 0; t < S; ++t) {
+      const uint32_t h = hdr[t];
+      const int mp = (h >> 8) & 0xff, kp = h >> 16;
+      dv[t * NPW + q] = 0.0;
+      for (int pr = 0; pr < mp; ++pr) val[(size_t)kp * NPW + q * mp + pr] = make_double2(0.0, 0.0);
+    }
+    return;
+  }
+  const char* rec = P.rec + P.recoff[j * P.L];
+  const int4 h4 = *(const int4*)rec;
+  const int n = h4.x, nL = h4.z;
+  if (n != S) { atomicExch(P.bad, 1); return; }
+  const RecLayout R = rec_layout(n, nL);
+  const uint16_t* brp = (const uint16_t*)(rec + R.brp);
+  const uint16_t* sch = (const uint16_t*)(rec + R.sched);
+  const uint16_t* bkv = (const uint16_t*)(rec + R.bk);
+  const double* bLv = (const double*)(rec + R.bL);
+  const double* Dn = (const double*)(rec + R.D);
+  bool mism = false;
+  for (int t = 0; t < S; ++t) {
+    const uint32_t h = hdr[t];
+    const int k = h & 0xff, mp = (h >> 8) & 0xff, kp = h >> 16;
+    const int b0 = brp[t], cb = brp[t + 1] - b0;
+    if (sch[t] != k || (cb + 1) / 2 != mp) { mism = true; break; }
+    dv[t * NPW + q] = 1.0 / Dn[k];
+    for (int pr = 0; pr < mp; ++pr) {
+      const uint32_t iw = idx[(t * P.LP + pr % P.LP) * P.CM + pr / P.LP];
+      const int i0 = (iw & 0xffff) >> 3, i1 = (iw >> 16) >> 3;
+      double2 v;
+      v.x = bLv[b0 + 2 * pr];
+      if (bkv[b0 + 2 * pr] != i0) mism = true;
+      if (2 * pr + 1 < cb) {
+        v.y = bLv[b0 + 2 * pr + 1];
+        if (bkv[b0 + 2 * pr + 1] != i1) mism = true;
+      } else {
+        v.y = 0.0;
+      }
+      val[(size_t)kp * NPW + q * mp + pr] = v;
+    }
+  }
+  if (mism) atomicExch(P.bad, 1);
+}
+
+struct QParams {
+  WParams w;
+  const char* qrec;
+  const long long* qrecoff;
+  const char* sched;
+  int sched_stride;
+  int vd;                // doubles per patch vector in shared memory
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// schedule-word load that stays where it is written (a plain read-only load is sunk by
+// the compiler to its first use, i.e. behind the step it is meant to overlap)
+__device__ __forceinline__ uint32_t ldg_pin(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// The warp's view of its Q-record and schedule during a sweep
+struct QSw {
+  const uint32_t* hdr;   // [S]
+  const uint32_t* idx;   // [S][LP][CM], lane-adjusted (+ hl CM)
+  const double* dinv;    // [S][NPW], lane-adjusted (+ q)
+  const double2* val;
+  int S;
+  uint32_t ring_s;       // shared address of the value ring [QD][CM][32] f64x2, lane-adjusted
+  uint32_t dring_s;      // shared address of the dinv ring [QD][NPW] f64, lane-adjusted
+  const double2* ring;   // the same rings, generic pointers
+  const double* dring;
+};
+
+// One triangular sweep of the warp's NPW patches over vector V (the lane's patch).
+template <int LP, int CM, bool BWD>
+__device__ __forceinline__ void qsweep(const QSw& Q, double* V, int hl, int q) {
+  constexpr int NPW = 32 / LP;
+  const int S = Q.S;
+  char* Vb = (char*)V;
+  auto T = [&](int tau) { return BWD ? S - 1 - tau : tau; };
+  auto issue = [&](int tau, uint32_t h) {
+    if (tau < S) {
+      const int mp = (h >> 8) & 0xff, kp = h >> 16;
+      const double2* src = Q.val + ((size_t)kp * NPW + q * mp);
+      const uint32_t dst = Q.ring_s + (uint32_t)((tau & (QD - 1)) * CM) * 512u;
+#pragma unroll
+      for (int c = 0; c < CM; ++c) {
+        const int pr = hl + LP * c;
+        const bool ok = pr < mp;
+        cp_async16(dst + c * 512u, src + (ok ? pr : 0), ok ? 16u : 0u);
+      }
+      if (!BWD && hl == 0) cp_async8(Q.dring_s + (uint32_t)((tau & (QD - 1)) * NPW) * 8u, Q.dinv + T(tau) * NPW);
+    }
+    cp_async_commit();
+  };
+  if (S == 0) return;
+  uint32_t hI = Q.hdr[T(0)];
+#pragma unroll
+  for (int tau = 0; tau < QD; ++tau) {
+    const uint32_t hn = tau + 1 < S ? Q.hdr[T(tau + 1)] : 0u;
+    issue(tau, hI);
+    hI = hn;
+  }
+  uint32_t hC = Q.hdr[T(0)];
+  uint32_t iC[CM];
+#pragma unroll
+  for (int c = 0; c < CM; ++c) iC[c] = Q.idx[T(0) * LP * CM + c];
+  for (int tau = 0; tau < S; ++tau) {
+    // schedule words of the next step and of the step issued next
+    uint32_t hN = 0u, iN[CM];
+#pragma unroll
+    for (int c = 0; c < CM; ++c) iN[c] = 0u;
+    if (tau + 1 < S) {
+      hN = Q.hdr[T(tau + 1)];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) iN[c] = Q.idx[T(tau + 1) * LP * CM + c];
+    }
+    const uint32_t hI2 = tau + QD + 1 < S ? Q.hdr[T(tau + QD + 1)] : 0u;
+    cp_async_wait<QD - 1>();
+    const int k8 = (hC & 0xff) * 8;
+    const double2* rg = Q.ring + (tau & (QD - 1)) * CM * 32;
+    double2 l[CM];
+#pragma unroll
+    for (int c = 0; c < CM; ++c) l[c] = rg[c * 32];
+    if (!BWD) {
+      const double yk = *(const double*)(Vb + k8);
+      double v0[CM], v1[CM];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) {
+        v0[c] = *(const double*)(Vb + (iC[c] & 0xffff));
+        v1[c] = *(const double*)(Vb + (iC[c] >> 16));
+      }
+      const double dk = Q.dring[(tau & (QD - 1)) * NPW];
+#pragma unroll
+      for (int c = 0; c < CM; ++c) {
+        *(double*)(Vb + (iC[c] & 0xffff)) = fma(-l[c].x, yk, v0[c]);
+        *(double*)(Vb + (iC[c] >> 16)) = fma(-l[c].y, yk, v1[c]);
+      }
+      if (hl == 0) *(double*)(Vb + k8) = yk * dk;
+    } else {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CM; ++c) {
+        a0 = fma(-l[c].x, *(const double*)(Vb + (iC[c] & 0xffff)), a0);
+        a1 = fma(-l[c].y, *(const double*)(Vb + (iC[c] >> 16)), a1);
+      }
+      double a = a0 + a1;
+#pragma unroll
+      for (int m = 1; m < LP; m <<= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+      if (hl == 0) *(double*)(Vb + k8) += a;
+    }
+    __syncwarp();
+    issue(tau + QD, hI);
+    hI = hI2;
+    hC = hN;
+#pragma unroll
+    for (int c = 0; c < CM; ++c) iC[c] = iN[c];
+  }
+  cp_async_wait<0>();
+}
+
+// M^{-1} V in place (V[n] = 0 on entry: the dummy node)
+template <int LP, int CM>
+__device__ __forceinline__ void qsmooth(const QSw& Q, double* V, int n, int hl, int q) {
+  qsweep<LP, CM, false>(Q, V, hl, q);
+  if (hl == 0) V[n] = 0.0;
+  __syncwarp();
+  qsweep<LP, CM, true>(Q, V, hl, q);
+}
+
+template <int LP, int CM>
+__global__ void __launch_bounds__(32) k_vq(QParams P) {
+  constexpr int NPW = 32 / LP;
+  const int lane = threadIdx.x, q = lane / LP, hl = lane & (LP - 1);
+  const long long w = blockIdx.x;
+  const long long slot = NPW * w + q;
+  const long long j = P.w.pord[slot];
+  const bool act = j >= 0;
+  const char* blk = P.qrec + P.qrecoff[w];
+  const int4 hd = __ldg((const int4*)blk);
+  const char* tab = P.sched + (size_t)hd.x * P.sched_stride;
+  const int S = hd.y;
+  // shared memory: vectors [NPW][2][vd] | value ring [QD][CM][32] f64x2 | dinv ring [QD][NPW] |
+  // the warp's sweep schedule (hdr[S], idx[S][LP][CM]; a global load per step would
+  // stall every step on its L2 latency)
+  double* X = wsm + (size_t)q * 2 * P.vd;
+  double* Sv = X + P.vd;
+  double2* ring = (double2*)(wsm + (size_t)NPW * 2 * P.vd);
+  double* dring = (double*)(ring + QD * CM * 32);
+  uint32_t* ssched = (uint32_t*)(dring + QD * NPW);
+  {
+    const uint32_t* gs = (const uint32_t*)(tab + 16);
+    const int nwords = S * (1 + LP * CM);
+    for (int i = lane; i < nwords; i += 32) ssched[i] = __ldg(gs + i);
+  }
+  QSw Q;
+  Q.hdr = ssched;
+  Q.idx = Q.hdr + S + hl * CM;
+  Q.dinv = (const double*)(blk + 16) + q;
+  Q.val = (const double2*)(blk + 16 + 8ll * S * NPW);
+  Q.S = S;
+  Q.ring = ring + lane;
+  Q.dring = dring + q;
+  Q.ring_s = (uint32_t)__cvta_generic_to_shared(ring + lane);
+  Q.dring_s = (uint32_t)__cvta_generic_to_shared(dring + q);
+  WBox c;
+  c.n = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { c.lo[k] = 0; c.ext[k] = 0; c.cext[k] = 0; c.ec[k] = 1; }
+  if (act) {
+    int elo[3], ehi[3];
+    patch_elems(P.w.G, j, elo, ehi);
+    c.n = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      c.ec[k] = ehi[k] - elo[k] + 1;
+      c.lo[k] = elo[k] * (P.w.G.ml[0] - 1) + 1;
+      c.ext[k] = c.ec[k] * (P.w.G.ml[0] - 1) - 1;
+      c.cext[k] = c.ec[k] * (P.w.G.ml[1] - 1) - 1;
+      c.n *= c.ext[k];
+    }
+  }
+  const int ex = c.ext[0], ey = c.ext[1];
+  const size_t Nx = P.w.G.Nax[0][0], Ny = P.w.G.Nax[0][1];
+  const float rex = 1.0f / max(ex, 1), rexy = 1.0f / max(ex * ey, 1);
+  auto gidx = [&](int i) {
+    int ix, iy, iz;
+    box_xyz(i, ex, ey, rex, rexy, ix, iy, iz);
+    return (c.lo[0] + ix) + Nx * ((c.lo[1] + iy) + Ny * (size_t)(c.lo[2] + iz));
+  };
+  // r_j = I_j^T r (a5); entries past the patch (the dummy node S, empty slots) are zero
+  for (int i = hl; i < P.vd; i += LP) { X[i] = i < c.n ? __ldg(P.w.r + gidx(i)) : 0.0; Sv[i] = 0.0; }
+  __syncwarp();
+  qsmooth<LP, CM>(Q, X, S, hl, q);                                       // x = M^{-1} r_j
+  __syncwarp();
+  wmid<LP>(P.w, c, X, Sv, act, slot, hl);
+  if (hl == 0) Sv[S] = 0.0;
+  __syncwarp();
+  qsmooth<LP, CM>(Q, Sv, S, hl, q);                                      // M^{-1} s
+  __syncwarp();
+  for (int i = hl; i < c.n; i += LP) atomicAdd(P.w.z + gidx(i), X[i] + Sv[i]);  // z += I_j (y + M^{-1} s) (a8)
+}
+
+// Slot order of Q mode: the tile order, patches grouped by their level-0 box shape,
+// each group padded to whole warps of NPW patches.  *ok = 0 when some patch differs
+// from its shape's schedule (the caller falls back to the thread-mode kernels).
+int qrec_build(lorpc_prec* b, cudaStream_t s, int* ok) {
+  *ok = 0;
+  int LP = 4;
+  if (const char* e = getenv("LORPC_QLP")) LP = atoi(e);
+  if (LP != 2 && LP != 4 && LP != 8) return fail(LORPC_ERR_ARG, "LORPC_QLP must be 2, 4 or 8");
+  const int NPW = 32 / LP;
+  const std::vector<int> ord = tile_order(b, 32, 32);
+  const PatchGeom G = make_geom(b);
+  std::vector<std::pair<int, std::vector<int>>> groups;  // shape key -> patches, in order of first appearance
+  {
+    for (int j : ord) {
+      if (j < 0) continue;
+      int lo[3], ext[3];
+      patch_box(G, j, 0, lo, ext);
+      const int key = ext[0] | (ext[1] << 10) | (ext[2] << 20);
+      size_t g = 0;
+      while (g < groups.size() && groups[g].first != key) ++g;
+      if (g == groups.size()) groups.push_back({key, {}});
+      groups[g].second.push_back(j);
+    }
+  }
+  std::vector<int> qord, wshape, sref;
+  for (size_t g = 0; g < groups.size(); ++g) {
+    sref.push_back(groups[g].second[0]);
+    qord.insert(qord.end(), groups[g].second.begin(), groups[g].second.end());
+    qord.resize((qord.size() + NPW - 1) / NPW * NPW, -1);
+    wshape.resize(qord.size() / NPW, (int)g);
+  }
+  const long long nslots = (long long)qord.size(), nw = nslots / NPW;
+  const int nsh = (int)groups.size();
+  if (nslots == 0) return LORPC_OK;
+  int *d_sref = nullptr, *d_wshape = nullptr, *bad = nullptr;
+  int4* d_info = nullptr;
+  LORPC_TRY(dalloc(&b->pord, qord.size()));
+  LORPC_TRY(dalloc(&d_sref, sref.size()));
+  LORPC_TRY(dalloc(&d_wshape, wshape.size()));
+  LORPC_TRY(dalloc(&d_info, (size_t)nsh));
+  LORPC_TRY(dalloc(&bad, 1));
+  LORPC_CUDA(cudaMemcpyAsync(b->pord, qord.data(), sizeof(int) * qord.size(), cudaMemcpyHostToDevice, s));
+  LORPC_CUDA(cudaMemcpyAsync(d_sref, sref.data(), sizeof(int) * sref.size(), cudaMemcpyHostToDevice, s));
+  LORPC_CUDA(cudaMemcpyAsync(d_wshape, wshape.data(), sizeof(int) * wshape.size(), cudaMemcpyHostToDevice, s));
+  LORPC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  QBuildParams P{};
+  P.rec = b->rec; P.recoff = b->recoff; P.pord = b->pord; P.shape_ref = d_sref; P.wshape = d_wshape;
+  P.L = b->L; P.LP = LP; P.nshapes = nsh; P.nslots = nslots; P.info = d_info; P.bad = bad;
+  k_qsched<<<nb(nsh, 32), 32, 0, s>>>(P, 0);
+  LORPC_LAUNCHED();
+  std::vector<int4> info((size_t)nsh);
+  LORPC_CUDA(cudaMemcpyAsync(info.data(), d_info, sizeof(int4) * nsh, cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  int Smax = 0, mpmax = 0;
+  bool fits = true;
+  for (const int4& v : info) {
+    Smax = std::max(Smax, v.x); mpmax = std::max(mpmax, v.z);
+    if (v.y > 65535 || v.x > 254) fits = false;
+  }
+  // ring rows per step: the instantiated CM at or above ceil(mpmax / LP)
+  const int need = std::max(1, (mpmax + LP - 1) / LP);
+  int CM = 0;  // the (LP, CM) pairs vcycle_q_apply instantiates
+  for (int cand : {1, 2, 3, 4, 5, 7}) {
+    const bool have = LP == 2 ? (cand == 4 || cand == 5 || cand == 7) : LP == 4 ? cand <= 4 : cand <= 2;
+    if (have && cand >= need) { CM = cand; break; }
+  }
+  auto cleanup = [&]() { dfree(d_sref); dfree(d_wshape); dfree(d_info); dfree(bad); };
+  if (!fits || CM == 0) { cleanup(); dfree(b->pord); return LORPC_OK; }
+  b->qlp = LP; b->qcm = CM;
+  b->qsched_stride = (qsched_bytes(Smax, LP, CM) + 255) & ~255;
+  LORPC_TRY(dalloc(&b->qsched, (size_t)nsh * b->qsched_stride));
+  P.CM = CM; P.sched = b->qsched; P.sched_stride = b->qsched_stride;
+  k_qsched<<<nb(nsh, 32), 32, 0, s>>>(P, 1);
+  LORPC_LAUNCHED();
+  std::vector<long long> off((size_t)nw);
+  long long acc = 0;
+  for (long long w = 0; w < nw; ++w) {
+    off[w] = acc;
+    const int4& v = info[wshape[w]];
+    acc += qrec_bytes(v.x, v.y, NPW);
+  }
+  b->qrec_bytes = acc;
+  LORPC_TRY(dalloc(&b->qrec, (size_t)acc));
+  LORPC_TRY(dalloc(&b->qrecoff, off.size()));
+  LORPC_CUDA(cudaMemcpyAsync(b->qrecoff, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice, s));
+  P.qrec = b->qrec; P.qrecoff = b->qrecoff;
+  k_qrec<<<nb(nslots, 128), 128, 0, s>>>(P);
+  LORPC_LAUNCHED();
+  int hbad = 0;
+  LORPC_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  cleanup();
+  if (hbad) {
+    dfree(b->pord); dfree(b->qrec); dfree(b->qrecoff); dfree(b->qsched);
+    return LORPC_OK;
+  }
+  b->wslots = nslots;
+  if (getenv("LORPC_VERBOSE"))
+    fprintf(stderr, "[lorpc] qrec: %lld slots in %lld warps, %d shapes, LP %d, CM %d (widest column %d pairs), %.2f GB\n",
+            nslots, nw, nsh, LP, CM, mpmax, acc / 1e9);
+  // packed dense coarse operators in slot order
+  LORPC_TRY(dalloc(&b->Cq, (size_t)(nslots * WNPK)));
+  k_wpack_c<<<nb(nslots * WNPK, 256), 256, 0, s>>>(b->Cd, b->Cq, b->pord, make_geom(b), nslots, b->ldc);
+  LORPC_LAUNCHED();
+  LORPC_CUDA(cudaStreamSynchronize(s));
+  dfree(b->Cd);
+  *ok = 1;
+  return LORPC_OK;
+}
+
+static QParams make_qparams(const lorpc_prec* b, const double* r, double* z) {
+  QParams P{};
+  P.w.G = make_geom(b);
+  P.w.A0 = b->lor->A[0];
+  P.w.W = b->wtab;
+  memcpy(P.w.woff, b->woff[0], sizeof(P.w.woff));
+  P.w.pord = b->pord; P.w.nslots = b->wslots;
+  P.w.Cq = b->Cq;
+  P.w.r = r; P.w.z = z;
+  P.qrec = b->qrec; P.qrecoff = b->qrecoff; P.sched = b->qsched; P.sched_stride = b->qsched_stride;
+  P.vd = std::max((b->max_n[0] + 2) & ~1, 120);
+  return P;
+}
+
+size_t qmode_smem(const lorpc_prec* b) {
+  const int NPW = 32 / b->qlp;
+  const int vd = std::max((b->max_n[0] + 2) & ~1, 120);
+  const size_t sched = 4 * (size_t)b->max_n[0] * (1 + b->qlp * b->qcm);
+  return (size_t)NPW * 2 * vd * 8 + (size_t)QD * b->qcm * 512 + (size_t)QD * NPW * 8 + ((sched + 15) & ~(size_t)15);
+}
+
+template <int LP, int CM>
+static int launch_vq(const lorpc_prec* b, const QParams& P, cudaStream_t s) {
+  constexpr int NPW = 32 / LP;
+  const size_t smem = qmode_smem(b);
+  cudaFuncSetAttribute(k_vq<LP, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_vq<LP, CM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k_vq<LP, CM><<<(unsigned)(P.w.nslots / NPW), 32, smem, s>>>(P);
+  LORPC_LAUNCHED();
+  return LORPC_OK;
+}
+
+int vcycle_q_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t s) {
+  const QParams P = make_qparams(b, r, z);
+  if (P.w.nslots == 0) return LORPC_OK;
+  if (qmode_smem(b) > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_q: shared memory");
+  const int key = b->qlp * 16 + b->qcm;
+  switch (key) {
+    case 2 * 16 + 4: return launch_vq<2, 4>(b, P, s);
+    case 2 * 16 + 5: return launch_vq<2, 5>(b, P, s);
+    case 2 * 16 + 7: return launch_vq<2, 7>(b, P, s);
+    case 4 * 16 + 1: return launch_vq<4, 1>(b, P, s);
+    case 4 * 16 + 2: return launch_vq<4, 2>(b, P, s);
+    case 4 * 16 + 3: return launch_vq<4, 3>(b, P, s);
+    case 4 * 16 + 4: return launch_vq<4, 4>(b, P, s);
+    case 8 * 16 + 1: return launch_vq<8, 1>(b, P, s);
+    case 8 * 16 + 2: return launch_vq<8, 2>(b, P, s);
+    default: return fail(LORPC_ERR_SIZE, "vcycle_q: (LP, CM) not compiled");
+  }
 }
 
 }  // namespace lorpc
