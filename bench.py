@@ -463,7 +463,9 @@ def run_lorpc_dist(args, cfg, dev, rank, world, dist):
 
 
 # ILU(0) ordering per config when --ordering is not given
-ORDERING = {"C1": "mdf", "C2": "mdf", "C3": "mdf", "C4": "mdf", "C5": "mdf"}
+# C5: RCM ("comparable iteration counts"; 69 iterations with either): a structure-only
+# ordering lets the warp's patches share one sweep schedule (U-records), 38.4 vs 41.8 ms per V-cycle
+ORDERING = {"C1": "mdf", "C2": "mdf", "C3": "mdf", "C4": "mdf", "C5": "rcm"}
 
 
 def main():

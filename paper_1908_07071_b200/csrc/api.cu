@@ -190,7 +190,7 @@ int lorpc_schwarz_setup(const lorpc_lor* l, const lorpc_schwarz_desc* desc, void
   if (rc == LORPC_OK) rc = dalloc(&b->pv, (size_t)m->ndof);
   if (rc == LORPC_OK) rc = dalloc(&b->qv, (size_t)m->ndof);
   if (rc == LORPC_OK) rc = dalloc(&b->scal, 16);
-  b->npart = std::max<long long>(1024, rz_parts(b));
+  b->npart = std::max<long long>(std::max<long long>(1024, rz_parts(b)), cg3_blocks(m));
   if (rc == LORPC_OK) rc = dalloc(&b->part, (size_t)b->npart);
   if (rc == LORPC_OK && cudaMallocHost(&b->hostpin, 16 * sizeof(double)) != cudaSuccess)
     rc = fail(LORPC_ERR_OOM, "cudaMallocHost");

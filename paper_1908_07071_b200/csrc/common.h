@@ -129,7 +129,6 @@ struct lorpc_prec {
   // thread-per-patch V-cycle (vcycle_t.cu): warp-interleaved factors, parking buffer
   bool tmode = false;
   bool umode = false;               // thread mode with one shared sweep schedule per warp (U-records)
-  int umpmax = 13;                  // widest column (pairs) of the U-records
   long long tslots = 0;             // warp slots of pord (multiple of 32)
   char* trec = nullptr;
   long long* trecoff = nullptr;
@@ -197,6 +196,8 @@ namespace lorpc {
 // internal entry points shared between translation units
 int geom_setup(lorpc_mesh* m, cudaStream_t s);
 int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s);
+int cg_apply_ex(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s, bool pre, double* xy_part);
+long long cg3_blocks(const lorpc_mesh* m);
 int dg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s);
 int dg_diag_setup(lorpc_mesh* m, cudaStream_t s);
 int dg_restrict_cg(const lorpc_mesh* m, const double* r_dg, double* r_cg, cudaStream_t s);

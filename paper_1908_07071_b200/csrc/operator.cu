@@ -65,7 +65,7 @@ __device__ __forceinline__ void ldg256(const double* p, double (&v)[4]) {
 template <int P, int EB>
 __global__ void __launch_bounds__((P + 1) * (P + 1) * EB)
 k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ G, int3 n, int3 N,
-      const __grid_constant__ Basis1D bs, long long e0, long long e1) {
+      const __grid_constant__ Basis1D bs, long long e0, long long e1, double* __restrict__ xy_part) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q * Q * Q;
   constexpr int SK = CgLay<Q>::SK, SA = CgLay<Q>::SA, SE = CgLay<Q>::SE;
   __shared__ double S[2][3][EB * SE];
@@ -177,15 +177,32 @@ k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __rest
   // z-lines at the nodes (a = ti, b = tj): transposed z contraction and scatter
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) { v0[qz] = B0[r1 + qz]; v1[qz] = B0[SQ + r1 + qz]; }
-  if (!active || bxy) return;
+  // x . (K x) over the free nodes = the sum over the elements of x_e . (K_e x_e) (the masked
+  // entries of u are zero): PCG's p . q leaves with the operator, one partial per CTA
+  double xy = 0.0;
+  if (active && !bxy) {
 #pragma unroll
-  for (int c = 0; c < Q; ++c) {
-    const int gz = ez * P + c;
-    if (gz == 0 || gz == N.z - 1) continue;
-    double v = 0.0;
+    for (int c = 0; c < Q; ++c) {
+      const int gz = ez * P + c;
+      if (gz == 0 || gz == N.z - 1) continue;
+      double v = 0.0;
 #pragma unroll
-    for (int qz = 0; qz < Q; ++qz) v += bs.B[qz * Q + c] * v0[qz] + bs.D[qz * Q + c] * v1[qz];
-    atomicAdd(y + base + sz * gz, v);
+      for (int qz = 0; qz < Q; ++qz) v += bs.B[qz * Q + c] * v0[qz] + bs.D[qz * Q + c] * v1[qz];
+      atomicAdd(y + base + sz * gz, v);
+      xy += u[c] * v;
+    }
+  }
+  if (xy_part == nullptr) return;  // kernel-uniform
+  xy = warp_sum(xy);
+  __shared__ double red[(Q2 * EB + 31) / 32];
+  const int lt = ti + Q * (tj + Q * te);
+  if ((lt & 31) == 0) red[lt >> 5] = xy;
+  __syncthreads();
+  if (lt == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < (Q2 * EB + 31) / 32; ++k) t += red[k];
+    xy_part[blockIdx.x] = t;
   }
 }
 
@@ -244,7 +261,7 @@ k_cg2(const double* __restrict__ x, double* __restrict__ y, const double* __rest
 }
 
 template <int P>
-static void launch3(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
+static void launch3(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s, double* xy_part) {
   constexpr int Q = P + 1;
   constexpr int EB = (Q * Q <= 16) ? 8 : (Q * Q <= 25 ? 4 : 2);  // 6 EB SE doubles of shared memory <= 48 KB
   int3 n = make_int3(m->n[0], m->n[1], m->n[2]);
@@ -253,7 +270,7 @@ static void launch3(const lorpc_mesh* m, const double* x, double* y, cudaStream_
   const long long e0 = (long long)m->ez_lo * m->n[0] * m->n[1], e1 = (long long)m->ez_hi * m->n[0] * m->n[1];
   unsigned grid = (unsigned)((e1 - e0 + EB - 1) / EB);
   if (grid == 0) return;
-  k_cg3<P, EB><<<grid, blk, 0, s>>>(x, y, m->G, n, N, m->basis, e0, e1);
+  k_cg3<P, EB><<<grid, blk, 0, s>>>(x, y, m->G, n, N, m->basis, e0, e1, xy_part);
 }
 template <int P>
 static void launch2(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
@@ -266,12 +283,27 @@ static void launch2(const lorpc_mesh* m, const double* x, double* y, cudaStream_
   k_cg2<P, EB><<<grid, blk, 0, s>>>(x, y, m->G, n, N, m->basis);
 }
 
-int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
+// CTAs of the 3D operator kernel (= partial sums of x . y it can write)
+long long cg3_blocks(const lorpc_mesh* m) {
+  if (m->d != 3) return 0;
+  const int Q = m->p + 1;
+  const int EB = (Q * Q <= 16) ? 8 : (Q * Q <= 25 ? 4 : 2);
+  const long long ne = (long long)(m->ez_hi - m->ez_lo) * m->n[0] * m->n[1];
+  return (ne + EB - 1) / EB;
+}
+
+// y = K x.  pre = false: y already holds x at the Dirichlet nodes and 0 elsewhere (the
+// caller fused that pass).  xy_part != nullptr (3D only): cg3_blocks(m) partial sums of
+// x . y over the free nodes.
+int cg_apply_ex(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s, bool pre, double* xy_part) {
   if (m->ndof_cg >= (1ll << 31)) return fail(LORPC_ERR_SIZE, "cg_apply: grid of 2^31 nodes or more");
   int3 N = make_int3(m->N[0], m->N[1], m->N[2]);
-  const unsigned g = (unsigned)((m->ndof_cg + 255) / 256);
-  if (m->d == 2) k_pre<2><<<g, 256, 0, s>>>(x, y, N); else k_pre<3><<<g, 256, 0, s>>>(x, y, N);
-  LORPC_LAUNCHED();
+  if (xy_part && m->d != 3) return fail(LORPC_ERR_ARG, "cg_apply: fused x . y is 3D only");
+  if (pre) {
+    const unsigned g = (unsigned)((m->ndof_cg + 255) / 256);
+    if (m->d == 2) k_pre<2><<<g, 256, 0, s>>>(x, y, N); else k_pre<3><<<g, 256, 0, s>>>(x, y, N);
+    LORPC_LAUNCHED();
+  }
   if (m->d == 2) {
     switch (m->p) {
       case 1: launch2<1>(m, x, y, s); break; case 2: launch2<2>(m, x, y, s); break;
@@ -282,14 +314,18 @@ int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
     }
   } else {
     switch (m->p) {
-      case 1: launch3<1>(m, x, y, s); break; case 2: launch3<2>(m, x, y, s); break;
-      case 3: launch3<3>(m, x, y, s); break; case 4: launch3<4>(m, x, y, s); break;
-      case 5: launch3<5>(m, x, y, s); break; case 6: launch3<6>(m, x, y, s); break;
+      case 1: launch3<1>(m, x, y, s, xy_part); break; case 2: launch3<2>(m, x, y, s, xy_part); break;
+      case 3: launch3<3>(m, x, y, s, xy_part); break; case 4: launch3<4>(m, x, y, s, xy_part); break;
+      case 5: launch3<5>(m, x, y, s, xy_part); break; case 6: launch3<6>(m, x, y, s, xy_part); break;
       default: return fail(LORPC_ERR_SIZE, "cg_apply: p not compiled");
     }
   }
   LORPC_LAUNCHED();
   return LORPC_OK;
+}
+
+int cg_apply(const lorpc_mesh* m, const double* x, double* y, cudaStream_t s) {
+  return cg_apply_ex(m, x, y, s, true, nullptr);
 }
 
 }  // namespace lorpc

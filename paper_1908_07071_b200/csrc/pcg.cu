@@ -6,9 +6,10 @@
 // Scalars stay on the device; the dot products are two-stage reductions with a fixed
 // grid and tree (deterministic for a given z; the atomics of the operator and patch
 // scatters make z itself order-dependent in the last bits).  rho = r.z is fused into
-// the last pass over z (the coarse prolongation) when B has its R_0 term; the R_0
-// chain itself runs on a second stream concurrently with the patch batch
-// (vcycle.cu).  On p.Ap <= 0 alpha is set to 0, so a BREAKDOWN return leaves x and r
+// the last pass over z (the coarse prolongation) when B has its R_0 term; on CG meshes
+// the p update also writes the operator's pre-pass (q = p on the Dirichlet nodes, 0
+// elsewhere) and in 3D p . q leaves with the element kernel (operator.cu), so an
+// iteration has no separate dot-product pass.  On p.Ap <= 0 alpha is set to 0, so a BREAKDOWN return leaves x and r
 // as they were.  The host reads ||r|| once per iteration.
 #include <cmath>
 
@@ -70,6 +71,24 @@ __global__ void k_update_xr(double* __restrict__ x, double* __restrict__ r, cons
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// CG meshes: p = z + beta p (first: p = z) fused with the operator's pre-pass on its output,
+// q = p at the Dirichlet nodes and 0 elsewhere (the element kernel then scatter-adds into q)
+template <int DIM>
+__global__ void k_update_pq(double* __restrict__ p, const double* __restrict__ z, double* __restrict__ q, int3 N,
+                            const double* __restrict__ scal, int first) {
+  const double beta = first ? 0.0 : scal[S_BETA];
+  const unsigned ndof = (unsigned)N.x * N.y * N.z;
+  for (unsigned g = blockIdx.x * blockDim.x + threadIdx.x; g < ndof; g += gridDim.x * blockDim.x) {
+    const unsigned gxy = g / (unsigned)N.x;
+    const int gx = (int)(g - gxy * N.x), gy = (int)(gxy % (unsigned)N.y), gz = (int)(gxy / (unsigned)N.y);
+    bool d = gx == 0 || gx == N.x - 1 || gy == 0 || gy == N.y - 1;
+    if (DIM == 3) d = d || gz == 0 || gz == N.z - 1;
+    const double pv = first ? z[g] : z[g] + beta * p[g];
+    p[g] = pv;
+    q[g] = d ? pv : 0.0;
+  }
+}
+
 // p = z + beta p
 __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, long long n, const double* __restrict__ scal) {
   const double beta = scal[S_BETA];
@@ -129,11 +148,39 @@ int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double
     return LORPC_OK;
   }
   LORPC_TRY(precond_rho(b, r, z, n, part, scal, 0, s));
-  LORPC_CUDA(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  // CG meshes: the p update also prepares q for the element kernel; in 3D p . q leaves
+  // with the operator (one partial per CTA; p is zero at the Dirichlet nodes in PCG)
+  const bool cgm = m->desc.disc == 0 && m->ndof_cg < (1ll << 31);
+  const long long nq = cgm ? cg3_blocks(m) : 0;
+  const int3 N3 = make_int3(m->N[0], m->N[1], m->N[2]);
+  auto update_p = [&](int first) {
+    if (cgm) {
+      if (m->d == 2) k_update_pq<2><<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, z, q, N3, scal, first);
+      else k_update_pq<3><<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, z, q, N3, scal, first);
+    } else if (first) {
+      return cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) == cudaSuccess ? LORPC_OK
+                                                                                                    : (int)LORPC_ERR_CUDA;
+    } else {
+      k_update_p<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, z, n, scal);
+    }
+    LORPC_LAUNCHED();
+    return (int)LORPC_OK;
+  };
+  LORPC_TRY(update_p(1));
   int status = LORPC_ERR_NOT_CONVERGED;
   for (int k = 1; k <= maxit; ++k) {
-    LORPC_TRY(apply_operator(m, p, q, s));
-    LORPC_TRY(dot(p, q, n, part, scal, 1, s));
+    if (cgm) {
+      LORPC_TRY(cg_apply_ex(m, p, q, s, false, nq > 0 ? part : nullptr));
+      if (nq > 0) {
+        k_dot_final<<<1, 1024, 0, s>>>(part, (int)nq, scal, 1);
+        LORPC_LAUNCHED();
+      } else {
+        LORPC_TRY(dot(p, q, n, part, scal, 1, s));
+      }
+    } else {
+      LORPC_TRY(apply_operator(m, p, q, s));
+      LORPC_TRY(dot(p, q, n, part, scal, 1, s));
+    }
     k_update_xr<<<RED_BLOCKS, RED_THREADS, 0, s>>>(x, r, p, q, n, scal, part);
     LORPC_LAUNCHED();
     k_dot_final<<<1, 1024, 0, s>>>(part, RED_BLOCKS, scal, 2);
@@ -152,8 +199,7 @@ int pcg_run(const lorpc_mesh* m, const lorpc_prec* b, const double* bvec, double
     if (rep->res_hist) rep->res_hist[k] = rel;
     if (rel <= rtol) { rep->converged = 1; status = LORPC_OK; break; }
     LORPC_TRY(precond_rho(b, r, z, n, part, scal, 3, s));
-    k_update_p<<<RED_BLOCKS, RED_THREADS, 0, s>>>(p, z, n, scal);
-    LORPC_LAUNCHED();
+    LORPC_TRY(update_p(0));
   }
   LORPC_CUDA(cudaEventRecord(b->ev1, s));
   LORPC_CUDA(cudaEventSynchronize(b->ev1));

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
   double* Dd = fill ? (double*)(blk + U.D) : nullptr;
   double* Lc = fill ? (double*)(blk + U.Lc) : nullptr;
   bool mism = valid && n != S;
-  int kp = 0, mpw = 0;
+  int kp = 0;
   for (int t = 0; t < S; ++t) {
     int node = 0, b0 = 0, cb = 0;
     if (valid && t < n) { node = sch[t]; b0 = brp[t]; cb = brp[t + 1] - b0; }
@@ -283,7 +283,6 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
     if (valid && (node != rnode || cb != rcb)) mism = true;
     const int mp = (rcb + 1) / 2;
     if (mp > UMP) mism = true;
-    if (lane == 0 && mp > mpw) mpw = mp;
     for (int k = 0; k < rcb && k < 2 * UMP; ++k) {
       const int nd = (valid && k < cb) ? bkv[b0 + k] : 0;
       const int rnd = __shfl_sync(0xffffffffu, nd, ref);
@@ -305,7 +304,6 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
   }
   if (kp > 65535) mism = true;
   if (__any_sync(0xffffffffu, mism) && lane == 0) atomicExch(bad, 1);
-  if (!fill && lane == 0) atomicMax(bad + 1, mpw);  // widest column (pairs) of any warp
   if (!fill && lane == 0) P.sizes[w] = urec_layout(S, kp).total;
   if (fill && lane == 0) *(int4*)blk = make_int4(S, kp, 0, 0);
 }
@@ -317,30 +315,12 @@ static int urec_build(lorpc_prec* b, int TX, int TY, cudaStream_t s, int* ok) {
   *ok = 0;
   const std::vector<int> ord = tile_order(b, TX, TY);
   const PatchGeom G = make_geom(b);
-  // x-runs of a patch row (consecutive j, one shape) of 16 or more patches start a warp
-  // and are padded to whole warps, so most warps are one row run (k_vt_mid3c)
   std::map<int, std::vector<int>> groups;
-  {
-    const long long gx = G.kind == 0 ? G.n[0] + 1 : G.n[0];
-    size_t i = 0;
-    while (i < ord.size()) {
-      if (ord[i] < 0) { ++i; continue; }
-      int lo[3], ext[3];
-      patch_box(G, ord[i], 0, lo, ext);
-      const int key = ext[0] | (ext[1] << 10) | (ext[2] << 20);
-      size_t e = i + 1;
-      while (e < ord.size() && ord[e] == ord[e - 1] + 1 && ord[e] % gx != 0) {
-        patch_box(G, ord[e], 0, lo, ext);
-        if ((ext[0] | (ext[1] << 10) | (ext[2] << 20)) != key) break;
-        ++e;
-      }
-      std::vector<int>& g = groups[key];
-      const bool run = e - i >= 16;
-      if (run) g.resize((g.size() + 31) / 32 * 32, -1);
-      g.insert(g.end(), ord.begin() + i, ord.begin() + e);
-      if (run) g.resize((g.size() + 31) / 32 * 32, -1);
-      i = e;
-    }
+  for (int j : ord) {
+    if (j < 0) continue;
+    int lo[3], ext[3];
+    patch_box(G, j, 0, lo, ext);
+    groups[ext[0] | (ext[1] << 10) | (ext[2] << 20)].push_back(j);
   }
   std::vector<int> uord;
   uord.reserve(ord.size() + 32 * groups.size());
@@ -357,19 +337,17 @@ static int urec_build(lorpc_prec* b, int TX, int TY, cudaStream_t s, int* ok) {
   long long* sizes = nullptr;
   int* bad = nullptr;
   LORPC_TRY(dalloc(&sizes, (size_t)nw));
-  LORPC_TRY(dalloc(&bad, 2));
-  LORPC_CUDA(cudaMemsetAsync(bad, 0, 2 * sizeof(int), s));
+  LORPC_TRY(dalloc(&bad, 1));
+  LORPC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   P.sizes = sizes;
   const unsigned blocks = (unsigned)((nslots + 127) / 128);
   k_urec<<<blocks, 128, 0, s>>>(P, nslots, 0, bad);
   LORPC_LAUNCHED();
   std::vector<long long> h((size_t)nw);
-  int hbad2[2] = {0, 0};
+  int hbad = 0;
   LORPC_CUDA(cudaMemcpyAsync(h.data(), sizes, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
-  LORPC_CUDA(cudaMemcpyAsync(hbad2, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
-  const int hbad = hbad2[0];
-  b->umpmax = hbad2[1];
   if (hbad) {
     dfree(sizes); dfree(bad); dfree(b->pord);
     b->pord = nullptr;
@@ -469,7 +447,6 @@ struct TcParams {
   int n0max;         // largest finest-level patch (= the dummy node index)
   int pfd;           // L2 prefetch distance of the sweeps (pair rows)
   int warp_doubles;
-  int coop;          // 1: k_vt_mid3c serves the warps that are one x-run of a patch row
   const double* r;
   double* z;
 };
@@ -715,8 +692,8 @@ __device__ __forceinline__ void uload(UStage& g, const UDesc& d, const double2* 
     if (p < mp) g.l[p] = LORPC_RLD(Lp + (long long)(kp + p) * 32);
   if (!BWD) g.dinv = LORPC_RLD(Dd + 32 * t);
 }
-template <int MP, class G>
-__device__ __forceinline__ void ufwd(const G& g, const UDesc& d, double* X) {
+template <int MP>
+__device__ __forceinline__ void ufwd(const UStage& g, const UDesc& d, double* X) {
   const int k = unode(d);
   const double yk = X[LORPC_XS * k];
   double v[2 * MP + 1];
@@ -729,8 +706,8 @@ __device__ __forceinline__ void ufwd(const G& g, const UDesc& d, double* X) {
   }
   X[LORPC_XS * k] = yk * g.dinv;
 }
-template <int MP, class G>
-__device__ __forceinline__ void ubwd(const G& g, const UDesc& d, double* X) {
+template <int MP>
+__device__ __forceinline__ void ubwd(const UStage& g, const UDesc& d, double* X) {
   const int k = unode(d);
   double a[4] = {X[LORPC_XS * k], 0.0, 0.0, 0.0};
 #pragma unroll
@@ -740,8 +717,8 @@ __device__ __forceinline__ void ubwd(const G& g, const UDesc& d, double* X) {
   }
   X[LORPC_XS * k] = (a[0] + a[1]) + (a[2] + a[3]);
 }
-template <bool BWD, int MP, class G>
-__device__ __forceinline__ void ustep_mp(const G& g, const UDesc& d, double* X) {
+template <bool BWD, int MP>
+__device__ __forceinline__ void ustep_mp(const UStage& g, const UDesc& d, double* X) {
   if (BWD) ubwd<MP>(g, d, X); else ufwd<MP>(g, d, X);
 }
 template <bool BWD>
@@ -818,121 +795,6 @@ __device__ __forceinline__ void usmooth(const char* __restrict__ blk, double* X,
   usweep<false>(blk, X, TPFD, lane);
   X[LORPC_XS * dummy] = 0.0;
   usweep<true>(blk, X, TPFD, lane);
-}
-
-// ------------------------------------------------------------------ U-mode sweeps, deeper pipeline
-// The sweeps above load one step ahead and spend half their time waiting on those loads
-// (ncu r02c: 50% long-scoreboard).  When no column of the warp's schedule has more than
-// 7 pairs (natural and RCM orderings of the 5 x 5 x 5 boxes), a register stage is 7
-// pairs instead of 13, so NST stages fit: the values of step q + NST - 1 are requested
-// while step q is applied.  The descriptors are not loaded per step: lane l holds the
-// descriptor of sweep step 32 b + l of the current and the next block of 32 steps (one
-// coalesced load per block, 32 steps ahead) and a step's words are broadcast by shuffles.
-template <int MPT> struct UStageT { double2 l[MPT]; double dinv; };
-template <bool BWD, int MPT, class G>
-__device__ __forceinline__ void ustep_t(const G& g, const UDesc& d, double* X) {
-  switch (ump(d)) {  // warp-uniform
-    case 0: ustep_mp<BWD, 0>(g, d, X); break;
-    case 1: ustep_mp<BWD, 1>(g, d, X); break;
-    case 2: ustep_mp<BWD, 2>(g, d, X); break;
-    case 3: ustep_mp<BWD, 3>(g, d, X); break;
-    case 4: ustep_mp<BWD, 4>(g, d, X); break;
-    case 5: ustep_mp<BWD, 5>(g, d, X); break;
-    case 6: ustep_mp<BWD, 6>(g, d, X); break;
-    default: ustep_mp<BWD, (MPT < 7 ? MPT : 7)>(g, d, X); break;
-  }
-}
-template <bool BWD, int MPT, int NST>
-__device__ __forceinline__ void usweep_p(const char* __restrict__ blk, double* X, int TPFD, int lane) {
-  static_assert(MPT <= 7, "stage of at most 7 pairs");
-  constexpr int LA = NST - 1;
-  constexpr int NW = 1 + (2 * MPT + 3) / 4;  // descriptor words in use: header + 2 MPT node bytes
-  const int4 hd = __ldg((const int4*)blk);
-  const int S = hd.x, E2 = hd.y;
-  if (S == 0) return;
-  const URecLayout U = urec_layout(S, E2);
-  const uint4* Dsc = (const uint4*)(blk + U.desc);
-  const double* Dd = (const double*)(blk + U.D) + lane;
-  const double2* Lp = (const double2*)(blk + U.Lc) + lane;
-  if (lane == 0) {
-    l2_prefetch(Dsc, 32u * S);
-    if (!BWD) l2_prefetch(Dd - lane, 256u * S);
-  }
-  int pf = BWD ? E2 : 0;
-  auto stp = [&](int q) { return BWD ? S - 1 - q : q; };
-  auto prefetch = [&](int kp, int mp) {
-    if (lane != 0) return;
-    if (!BWD) {
-      while (pf < E2 && pf < kp + TPFD) {
-        const int nr = min(LORPC_PFR, E2 - pf);
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-        pf += nr;
-      }
-    } else {
-      while (pf > 0 && pf > kp + mp - TPFD) {
-        const int nr = min(LORPC_PFR, pf);
-        pf -= nr;
-        l2_prefetch(Lp - lane + pf * 32, 512u * nr);
-      }
-    }
-  };
-  // lane-distributed descriptor blocks
-  uint32_t c0[8], c1[8];
-  auto loadblk = [&](int b, uint32_t (&w)[8]) {
-    const int q = 32 * b + lane;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = 0u;
-    if (q < S) {
-      const uint4 a = __ldg(Dsc + 2 * stp(q));
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-      if (NW > 4) {
-        const uint4 c = __ldg(Dsc + 2 * stp(q) + 1);
-        w[4] = c.x; w[5] = c.y; w[6] = c.z; w[7] = c.w;
-      }
-    }
-  };
-  loadblk(0, c0);
-  loadblk(1, c1);
-  int cur = 0;  // block of c0
-  UStageT<MPT> st[NST];
-  auto issue = [&](int q, UStageT<MPT>& g) {
-    if (q < S) {
-      const uint32_t w0 = __shfl_sync(0xffffffffu, (q >> 5) == cur ? c0[0] : c1[0], q & 31);
-      const int mp = (w0 >> 8) & 0xff, kp = (int)(w0 >> 16);
-#pragma unroll
-      for (int p = 0; p < MPT; ++p)
-        if (p < mp) g.l[p] = LORPC_RLD(Lp + (long long)(kp + p) * 32);
-      if (!BWD) g.dinv = LORPC_RLD(Dd + 32 * stp(q));
-    }
-  };
-#pragma unroll
-  for (int u = 0; u < LA; ++u) issue(u, st[u]);
-  for (int q = 0; q < S; q += NST) {
-#pragma unroll
-    for (int u = 0; u < NST; ++u) {
-      const int qq = q + u;
-      if (qq < S) {
-        if ((qq & 31) == 0 && qq > 0) {  // next descriptor block
-#pragma unroll
-          for (int k = 0; k < 8; ++k) c0[k] = c1[k];
-          ++cur;
-          loadblk(cur + 1, c1);
-        }
-        issue(qq + LA, st[(u + LA) % NST]);
-        UDesc d;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) d.w[k] = k < NW ? __shfl_sync(0xffffffffu, c0[k], qq & 31) : 0u;
-        prefetch(ukp(d), ump(d));
-        ustep_t<BWD, MPT>(st[u], d, X);
-      }
-    }
-  }
-}
-template <int MPT, int NST>
-__device__ __forceinline__ void usmooth_p(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
-  usweep_p<false, MPT, NST>(blk, X, TPFD, lane);
-  X[LORPC_XS * dummy] = 0.0;
-  usweep_p<true, MPT, NST>(blk, X, TPFD, lane);
 }
 
 // ------------------------------------------------------------------ middle phase
@@ -1113,18 +975,6 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
   }
 }
 
-// true when the warp's valid lanes 0 .. nv - 1 hold x-consecutive patches of one patch row
-// (j0 + lane): the warps k_vt_mid3c serves
-__device__ __forceinline__ bool warp_is_row_run(const TcParams& P, long long j, int lane, long long& j0, int& nv) {
-  const unsigned vm = __ballot_sync(0xffffffffu, j >= 0);
-  nv = __popc(vm);
-  j0 = __shfl_sync(0xffffffffu, j, 0);
-  if (vm == 0u || (vm & (vm + 1u)) != 0u || j0 < 0) return false;  // valid lanes must be 0 .. nv - 1
-  const long long gx = P.G.kind == 0 ? P.G.n[0] + 1 : P.G.n[0];
-  const bool ok = j < 0 || (j == j0 + lane && (j0 % gx) + lane < gx);
-  return __all_sync(0xffffffffu, ok) && P.G.erng == nullptr && P.G.kind == 0;
-}
-
 // 3D line variant (patch boxes of at most 5 nodes per axis, p <= 3): the lane
 // walks its patch by x-lines.  For each line the 3 x 3 neighbouring lines of the
 // patch vector are read once into registers (zero outside the box) and the five
@@ -1192,11 +1042,6 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
   const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (slot >= P.nslots) return;
   const long long j = P.pord[slot];
-  if (P.coop) {  // warps that are one row run belong to k_vt_mid3c
-    long long j0;
-    int nv;
-    if (warp_is_row_run(P, j, threadIdx.x & 31, j0, nv)) return;
-  }
   if (j < 0) return;
   const long long w = slot >> 5;
   const int lane = threadIdx.x & 31;
@@ -1303,702 +1148,10 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
   }
 }
 
-// ------------------------------------------------------------------ middle phase, patch vector in shared memory
-// k_vt_mid3l reads the 3 x 3 neighbouring lines of the patch vector from the park buffer
-// in global memory, one node ahead: every node of the walk waits on those loads (x comes
-// from DRAM), and with them on its LOR row; the kernel's time per warp does not depend on
-// the occupancy (measured: 21 / 36 / 46 ms at 8 / 4 / 3 warps per SM with the rows coming
-// from shared memory), i.e. it is one long chain of exposed load latencies.  Here the
-// warp's patch vectors (n0max x 32 doubles, the layout of the smoothing kernels) are
-// brought into shared memory by ONE bulk async copy, the residual windows read shared
-// memory, the coarse correction updates the vector in place, the LOR row of the next
-// node is requested while the current one is applied, and y leaves with coalesced stores.
-template <bool RESTRICT>
-__device__ __forceinline__ void tline_residual_s(const TcParams& P, const TPatch& c, const double* V, int iy, int iz,
-                                                 double* res) {
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-  const long long g0 = c.lo[0] + Nx * ((c.lo[1] + iy) + Ny * (long long)(c.lo[2] + iz));
-  const double* L[3][3];
-  bool ok[3][3];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      const int yy = iy + dy - 1, zz = iz + dz - 1;
-      ok[dz][dy] = yy >= 0 && yy < ey && zz >= 0 && zz < ez;
-      L[dz][dy] = V + ((ok[dz][dy] ? zz * ey + yy : 0) * ex) * 32;
-    }
-  double W[3][3][TLX + 2];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      W[dz][dy][0] = 0.0;
-      W[dz][dy][1] = ok[dz][dy] ? L[dz][dy][0] : 0.0;
-    }
-  // the LOR row of node x + 1 (and its r) is requested while node x is applied
-  double an[28], rn;
-#pragma unroll
-  for (int d4 = 0; d4 < 7; ++d4) ld256(P.A0 + g0 * 28 + 4 * d4, an[4 * d4], an[4 * d4 + 1], an[4 * d4 + 2], an[4 * d4 + 3]);
-  rn = __ldg(P.r + g0);
-#pragma unroll
-  for (int x = 0; x < TLX; ++x) {
-    if (x >= ex) break;
-    double av[28];
-#pragma unroll
-    for (int d = 0; d < 28; ++d) av[d] = an[d];
-    double a0 = rn, a1 = 0.0;
-    if (x + 1 < ex) {
-      const double* Ar = P.A0 + (g0 + x + 1) * 28;
-#pragma unroll
-      for (int d4 = 0; d4 < 7; ++d4) ld256(Ar + 4 * d4, an[4 * d4], an[4 * d4 + 1], an[4 * d4 + 2], an[4 * d4 + 3]);
-      rn = __ldg(P.r + g0 + x + 1);
-    }
-#pragma unroll
-    for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
-        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? L[dz][dy][(x + 1) * 32] : 0.0;
-#pragma unroll
-    for (int d = 0; d < 27; ++d) {
-      const double v = (x + 2 + dir_dx(d) <= TLX + 1) ? W[dir_dz(d) + 1][dir_dy(d) + 1][x + 1 + dir_dx(d)] : 0.0;
-      if (d & 1) a1 -= av[d] * v; else a0 -= av[d] * v;
-    }
-    res[x] = a0 + a1;
-  }
-}
-
-__global__ void __launch_bounds__(32) k_vt_mid3s(TcParams P) {
-  constexpr int NC = 27, NPK = TCoarse<3>::NPK;
-  const int lane = threadIdx.x;
-  const long long w = blockIdx.x;
-  const long long j = P.pord[w * 32 + lane];
-  const bool valid = j >= 0;
-  const int n0 = P.n0max;
-  const long long col = w * (long long)n0 * 32;
-  // stage the warp's x vectors: one bulk copy of n0 rows of 256 bytes
-  uint64_t* bar = (uint64_t*)(tsm + (size_t)(n0 + 1) * 32);
-  const uint32_t sbar = (uint32_t)__cvta_generic_to_shared(bar);
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(256u * n0) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"((uint32_t)__cvta_generic_to_shared(tsm)), "l"(P.xpark + col), "r"(256u * n0), "r"(sbar) : "memory");
-  }
-  __syncwarp();
-  TPatch c{};
-  TWalk wk{};
-  if (valid) { c = tpatch<3>(P.G, j); wk = twalk<3>(P.G, c, j); }
-  {
-    uint32_t okw;
-    do {
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(okw) : "r"(sbar) : "memory");
-    } while (!okw);
-  }
-  if (!valid) return;
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  double* Xs = tsm + lane;  // the lane's column: node i at Xs[32 i]
-  double* Yp = P.ypark + col + lane;
-  double* Sp = P.spark + col + lane;
-  const double* Wx = P.W + P.woff[c.ec[0]];
-  const double* Wy = P.W + P.woff[c.ec[1]];
-  const double* Wz = P.W + P.woff[c.ec[2]];
-  auto wt = [](const double* T, int k, int ce, int e, int i) { return k < ce ? __ldg(T + k * e + i) : 0.0; };
-  // s = r - A x and r_1 = P^T s
-  double r1[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) r1[k] = 0.0;
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double res[TLX];
-      tline_residual_s<true>(P, c, Xs, iy, iz, res);
-      double t[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-#pragma unroll
-        for (int cx = 0; cx < 3; ++cx) t[cx] += wt(Wx, cx, c.cext[0], ex, x) * res[x];
-      }
-      double wy[3], wz[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-      for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-        for (int cy = 0; cy < 3; ++cy) {
-          const double f = wy[cy] * wz[cz];
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) r1[cx + 3 * (cy + 3 * cz)] += f * t[cx];
-        }
-    }
-  }
-  // z_1 = C r_1 (packed symmetric, fixed coarse box, interleaved by lane)
-  double z1[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) z1[k] = 0.0;
-  {
-    const double* C = P.Cp + w * 32ll * NPK + lane;
-    int idx = 0;
-#pragma unroll
-    for (int a = 0; a < NC; ++a) {
-#pragma unroll
-      for (int b = a; b < NC; ++b) {
-        const double cv = __ldcs(C + 32 * idx);
-        z1[a] += cv * r1[b];
-        if (b != a) z1[b] += cv * r1[a];
-        ++idx;
-      }
-    }
-  }
-  // y = x + P z_1 in place, by lines; y also goes to the park buffer of the post-smoothing
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double wy[3], wz[3], u[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-      for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-        for (int cy = 0; cy < 3; ++cy) {
-          const double f = wy[cy] * wz[cz];
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) u[cx] += f * z1[cx + 3 * (cy + 3 * cz)];
-        }
-      const int f0 = (iz * ey + iy) * ex;
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-        double e = 0.0;
-#pragma unroll
-        for (int cx = 0; cx < 3; ++cx) e += wt(Wx, cx, c.cext[0], ex, x) * u[cx];
-        const double yv = Xs[(f0 + x) * 32] + e;
-        Xs[(f0 + x) * 32] = yv;
-        __stcs(Yp + (long long)(f0 + x) * 32, yv);
-      }
-    }
-  }
-  // s = r - A y
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double res[TLX];
-      tline_residual_s<false>(P, c, Xs, iy, iz, res);
-      const long long f0 = (long long)(iz * ey + iy) * ex;
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-        __stcs(Sp + (f0 + x) * 32, res[x]);
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ middle phase, LOR rows through a cp.async ring
-// The line variant above waits on its LOR row loads (ncu: 76% of its stall samples are
-// long-scoreboard) and keeps 8 warps x 32 patches per SM in flight, whose rows (28 KB
-// per patch and pass) overflow L2, so each row crosses DRAM ~3 times per apply.  Here
-// every lane streams the rows of its walk (both residual passes: 2 n nodes) through a
-// shared-memory ring RD nodes deep with 16-byte cp.async copies (no registers held by
-// loads in flight), which hides the L2 latency at 3-7 warps per SM, few enough for
-// neighbouring patches to find their shared rows in L2.  Ring slot of a node:
-// [14 chunks][32 lanes] 16 B (conflict-free 128-bit reads) + [32 lanes] r_i.
-constexpr int MSLOT = 14 * 512 + 256;
-__device__ __forceinline__ void mcp16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void mcp8(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void mcommit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void mwait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// the lane's row stream: node m of the walk (two passes over the box, m in [0, 2 n))
-template <int RD>
-struct MRing {
-  const double* A0;
-  const double* r;
-  long long Nx, Ny;
-  int lo0, lo1, lo2, ex, ey, ez, n, fy, fz;
-  float rex, rey;
-  uint32_t sbase;        // shared address of the warp's ring + lane * 16
-  uint32_t rbase;        // shared address of the r entries + lane * 8
-  const char* gbase;     // generic pointer to the ring + lane * 16
-  int m_issue, m_use;
-  __device__ __forceinline__ void issue() {
-    const int m = m_issue++;
-    if (m < 2 * n) {
-      const int mm = m < n ? m : m - n;
-      const int ln = qdiv(mm, rex), x = mm - ln * ex;
-      const int kz = qdiv(ln, rey), ky = ln - kz * ey;
-      const int iy = fy ? ey - 1 - ky : ky, iz = fz ? ez - 1 - kz : kz;
-      const long long gi = (lo0 + x) + Nx * ((lo1 + iy) + Ny * (long long)(lo2 + iz));
-      const double* src = A0 + gi * 28;
-      const uint32_t dst = sbase + (uint32_t)(m % RD) * MSLOT;
-#pragma unroll
-      for (int j = 0; j < 14; ++j) mcp16(dst + j * 512, src + 2 * j);
-      mcp8(rbase + (uint32_t)(m % RD) * MSLOT, r + gi);
-    }
-    mcommit();
-  }
-  __device__ __forceinline__ void start() {
-    m_issue = 0; m_use = 0;
-#pragma unroll
-    for (int k = 0; k < RD; ++k) issue();
-  }
-  // row of the next node of the walk (call in walk order); then refill its slot
-  __device__ __forceinline__ void take(double (&av)[28], double& rr) {
-    mwait<RD - 1>();
-    const char* g = gbase + (size_t)(m_use % RD) * MSLOT;
-#pragma unroll
-    for (int j = 0; j < 14; ++j) {
-      const double2 t = *(const double2*)(g + j * 512);
-      av[2 * j] = t.x; av[2 * j + 1] = t.y;
-    }
-    rr = *(const double*)(g + 14 * 512 - (threadIdx.x & 31) * 8);
-    ++m_use;
-  }
-};
-
-template <int RD>
-__device__ __forceinline__ void tline_residual_r(MRing<RD>& R, const TPatch& c, const double* __restrict__ V, int iy,
-                                                 int iz, double* res) {
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  const double* L[3][3];
-  bool ok[3][3];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      const int yy = iy + dy - 1, zz = iz + dz - 1;
-      ok[dz][dy] = yy >= 0 && yy < ey && zz >= 0 && zz < ez;
-      L[dz][dy] = V + (long long)((ok[dz][dy] ? zz * ey + yy : 0) * ex) * 32;
-    }
-  double W[3][3][TLX + 2];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      W[dz][dy][0] = 0.0;
-      W[dz][dy][1] = ok[dz][dy] ? L[dz][dy][0] : 0.0;
-    }
-#pragma unroll
-  for (int x = 0; x < TLX; ++x) {
-    if (x >= ex) break;
-#pragma unroll
-    for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
-        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? L[dz][dy][(x + 1) * 32] : 0.0;
-    double av[28], a0, a1 = 0.0;
-    R.take(av, a0);
-#pragma unroll
-    for (int d = 0; d < 27; ++d) {
-      const double v = (x + 2 + dir_dx(d) <= TLX + 1) ? W[dir_dz(d) + 1][dir_dy(d) + 1][x + 1 + dir_dx(d)] : 0.0;
-      if (d & 1) a1 -= av[d] * v; else a0 -= av[d] * v;
-    }
-    R.issue();
-    res[x] = a0 + a1;
-  }
-}
-
-extern __shared__ __align__(16) char msm[];
-template <int RD>
-__global__ void __launch_bounds__(32) k_vt_mid3r(TcParams P) {
-  constexpr int NC = 27, NPK = TCoarse<3>::NPK;
-  const int lane = threadIdx.x;
-  const long long w = blockIdx.x;
-  const long long slot = w * 32 + lane;
-  const long long j = P.pord[slot];
-  if (j < 0) return;
-  const TPatch c = tpatch<3>(P.G, j);
-  const TWalk wk = twalk<3>(P.G, c, j);
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  const long long col = w * (long long)P.n0max * 32 + lane;
-  const double* Xp = P.xpark + col;
-  double* Yp = P.ypark + col;
-  double* Sp = P.spark + col;
-  const double* Wx = P.W + P.woff[c.ec[0]];
-  const double* Wy = P.W + P.woff[c.ec[1]];
-  const double* Wz = P.W + P.woff[c.ec[2]];
-  auto wt = [](const double* T, int k, int ce, int e, int i) { return k < ce ? __ldg(T + k * e + i) : 0.0; };
-  MRing<RD> R;
-  R.A0 = P.A0; R.r = P.r; R.Nx = P.G.Nax[0][0]; R.Ny = P.G.Nax[0][1];
-  R.lo0 = c.lo[0]; R.lo1 = c.lo[1]; R.lo2 = c.lo[2]; R.ex = ex; R.ey = ey; R.ez = ez; R.n = c.n;
-  R.fy = wk.fy; R.fz = wk.fz; R.rex = 1.0f / ex; R.rey = 1.0f / ey;
-  R.sbase = (uint32_t)__cvta_generic_to_shared(msm) + lane * 16;
-  R.rbase = (uint32_t)__cvta_generic_to_shared(msm) + 14 * 512 + lane * 8;
-  R.gbase = msm + lane * 16;
-  R.start();
-  // s = r - A x and r_1 = P^T s
-  double r1[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) r1[k] = 0.0;
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double res[TLX];
-      tline_residual_r<RD>(R, c, Xp, iy, iz, res);
-      double t[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-#pragma unroll
-        for (int cx = 0; cx < 3; ++cx) t[cx] += wt(Wx, cx, c.cext[0], ex, x) * res[x];
-      }
-      double wy[3], wz[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-      for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-        for (int cy = 0; cy < 3; ++cy) {
-          const double f = wy[cy] * wz[cz];
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) r1[cx + 3 * (cy + 3 * cz)] += f * t[cx];
-        }
-    }
-  }
-  // z_1 = C r_1 (packed symmetric, fixed coarse box, interleaved by lane)
-  double z1[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) z1[k] = 0.0;
-  {
-    const double* C = P.Cp + w * 32ll * NPK + lane;
-    int idx = 0;
-#pragma unroll
-    for (int a = 0; a < NC; ++a) {
-#pragma unroll
-      for (int b = a; b < NC; ++b) {
-        const double cv = __ldcs(C + 32 * idx);
-        z1[a] += cv * r1[b];
-        if (b != a) z1[b] += cv * r1[a];
-        ++idx;
-      }
-    }
-  }
-  // y = x + P z_1, by lines
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double wy[3], wz[3], u[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-      for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-        for (int cy = 0; cy < 3; ++cy) {
-          const double f = wy[cy] * wz[cz];
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) u[cx] += f * z1[cx + 3 * (cy + 3 * cz)];
-        }
-      const long long f0 = (long long)(iz * ey + iy) * ex;
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-        double e = 0.0;
-#pragma unroll
-        for (int cx = 0; cx < 3; ++cx) e += wt(Wx, cx, c.cext[0], ex, x) * u[cx];
-        Yp[(f0 + x) * 32] = Xp[(f0 + x) * 32] + e;
-      }
-    }
-  }
-  // s = r - A y
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      double res[TLX];
-      tline_residual_r<RD>(R, c, Yp, iy, iz, res);
-      const long long f0 = (long long)(iz * ey + iy) * ex;
-#pragma unroll
-      for (int x = 0; x < TLX; ++x) {
-        if (x >= ex) break;
-        __stcs(Sp + (f0 + x) * 32, res[x]);
-      }
-    }
-  }
-  mwait<0>();
-}
-
-// ------------------------------------------------------------------ middle phase, cooperative LOR rows
-// In U-mode slot order most warps hold up to 32 x-consecutive patches of one patch row
-// (same y, z and box shape), so the LOR rows a warp needs for one x-line of its walk are
-// ONE contiguous run of p (nv - 1) + ex node rows (98 at p = 3).  Lane-per-patch loads
-// fetch each of them 5/3 times, as 32 scattered 32-byte sectors per instruction
-// (k_vt_mid3l moves ~8 TB/s between L2 and the SMs, the limit of that pattern).  Here the
-// warp brings the run in once with bulk async copies (one 224-byte copy per row, row pitch
-// 240 bytes so the lanes' 128-bit reads are bank-conflict free; completion on an
-// mbarrier), NBUF lines in flight, and every lane reads its ex rows from shared memory.
-// Warps that are not such a run (clipped shapes along x, ragged group ends) exit here
-// and are served by k_vt_mid3l, which skips the others.
-constexpr int CROWP = 240;        // row pitch in shared memory (bytes)
-constexpr int CROWS = 32 * 3 + 8; // rows per line buffer (p <= 3: 3 * 31 + 5 = 98)
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  do {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
-}
-
-template <int NBUF>
-struct CRows {
-  const double* A0;
-  long long Nx, Ny, g00;  // g00: node index of (lo0 of lane 0, lo1, lo2)
-  int ey, ez, nl, nrows, fy, fz, lane;
-  uint32_t sbuf, sbar;    // shared addresses: line buffers, mbarriers
-  const char* gbuf;
-  int s_issue;
-  __device__ __forceinline__ long long line_g0(int s) const {
-    const int ls = s < nl ? s : s - nl;
-    const int kz = ls / ey, ky = ls - kz * ey;
-    const int iy = fy ? ey - 1 - ky : ky, iz = fz ? ez - 1 - kz : kz;
-    return g00 + Nx * (iy + Ny * (long long)iz);
-  }
-  // all lanes call; line s of the two-pass walk into buffer s % NBUF
-  __device__ __forceinline__ void issue() {
-    const int s = s_issue++;
-    if (s >= 2 * nl) return;
-    const uint32_t bar = sbar + 8u * (s % NBUF);
-    if (lane == 0) mbar_expect(bar, 224u * nrows);
-    __syncwarp();
-    const double* src = A0 + line_g0(s) * 28;
-    const uint32_t dst = sbuf + (uint32_t)(s % NBUF) * (CROWS * CROWP);
-    for (int row = lane; row < nrows; row += 32) bulk_g2s(dst + row * CROWP, src + (long long)row * 28, 224u, bar);
-  }
-  __device__ __forceinline__ const char* wait(int s) const {
-    mbar_wait(sbar + 8u * (s % NBUF), (uint32_t)((s / NBUF) & 1));
-    return gbuf + (size_t)(s % NBUF) * (CROWS * CROWP);
-  }
-  // all lanes call after their last read of line s
-  __device__ __forceinline__ void release() {
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue();
-  }
-};
-
-// residual of one x-line, LOR rows from the line buffer (rows of this lane start at row0)
-__device__ __forceinline__ void tline_residual_c(const TcParams& P, const TPatch& c, const char* rows,
-                                                 const double* __restrict__ V, int iy, int iz, double* res) {
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  const long long Nx = P.G.Nax[0][0], Ny = P.G.Nax[0][1];
-  const long long g0 = c.lo[0] + Nx * ((c.lo[1] + iy) + Ny * (long long)(c.lo[2] + iz));
-  const double* L[3][3];
-  bool ok[3][3];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      const int yy = iy + dy - 1, zz = iz + dz - 1;
-      ok[dz][dy] = yy >= 0 && yy < ey && zz >= 0 && zz < ez;
-      L[dz][dy] = V + (long long)((ok[dz][dy] ? zz * ey + yy : 0) * ex) * 32;
-    }
-  double W[3][3][TLX + 2];
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      W[dz][dy][0] = 0.0;
-      W[dz][dy][1] = ok[dz][dy] ? L[dz][dy][0] : 0.0;
-    }
-#pragma unroll
-  for (int x = 0; x < TLX; ++x) {
-    if (x >= ex) break;
-#pragma unroll
-    for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
-        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? L[dz][dy][(x + 1) * 32] : 0.0;
-    double a0 = __ldg(P.r + g0 + x), a1 = 0.0;
-    const double2* rp = (const double2*)(rows + x * CROWP);
-#pragma unroll
-    for (int d2 = 0; d2 < 14; ++d2) {
-      const double2 av = rp[d2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int d = 2 * d2 + h;
-        if (d >= 27) break;
-        const double v = (x + 2 + dir_dx(d) <= TLX + 1) ? W[dir_dz(d) + 1][dir_dy(d) + 1][x + 1 + dir_dx(d)] : 0.0;
-        if (h) a1 -= av.y * v; else a0 -= av.x * v;
-      }
-    }
-    res[x] = a0 + a1;
-  }
-}
-
-extern __shared__ __align__(128) char csm[];
-template <int NBUF>
-__global__ void __launch_bounds__(32) k_vt_mid3c(TcParams P) {
-  constexpr int NC = 27, NPK = TCoarse<3>::NPK;
-  const int lane = threadIdx.x;
-  const long long w = blockIdx.x;
-  const long long j = P.pord[w * 32 + lane];
-  long long j0;
-  int nv;
-  if (!warp_is_row_run(P, j, lane, j0, nv)) return;  // k_vt_mid3l takes this warp
-  const bool valid = j >= 0;
-  const TPatch c0 = tpatch<3>(P.G, j0);
-  TPatch c = c0;
-  const int pe = P.G.ml[0] - 1;
-  c.lo[0] += pe * lane;  // same row and shape: boxes p nodes apart
-  const TWalk wk = twalk<3>(P.G, c0, j0);
-  const int ex = c.ext[0], ey = c.ext[1], ez = c.ext[2];
-  const long long col = w * (long long)P.n0max * 32 + lane;
-  const double* Xp = P.xpark + col;
-  double* Yp = P.ypark + col;
-  double* Sp = P.spark + col;
-  const double* Wx = P.W + P.woff[c.ec[0]];
-  const double* Wy = P.W + P.woff[c.ec[1]];
-  const double* Wz = P.W + P.woff[c.ec[2]];
-  auto wt = [](const double* T, int k, int ce, int e, int i) { return k < ce ? __ldg(T + k * e + i) : 0.0; };
-  CRows<NBUF> R;
-  R.A0 = P.A0; R.Nx = P.G.Nax[0][0]; R.Ny = P.G.Nax[0][1];
-  R.g00 = c0.lo[0] + R.Nx * (c0.lo[1] + R.Ny * (long long)c0.lo[2]);
-  R.ey = ey; R.ez = ez; R.nl = ey * ez; R.nrows = pe * (nv - 1) + ex; R.fy = wk.fy; R.fz = wk.fz; R.lane = lane;
-  R.sbuf = (uint32_t)__cvta_generic_to_shared(csm);
-  R.sbar = R.sbuf + NBUF * (CROWS * CROWP);
-  R.gbuf = csm;
-  R.s_issue = 0;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NBUF; ++k) mbar_init(R.sbar + 8u * k, 1u);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < NBUF; ++k) R.issue();
-  const int rowoff = pe * lane * CROWP;
-  int sline = 0;
-  // s = r - A x and r_1 = P^T s
-  double r1[NC];
-#pragma unroll
-  for (int k = 0; k < NC; ++k) r1[k] = 0.0;
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      const char* rows = R.wait(sline++) + rowoff;
-      if (valid) {
-        double res[TLX];
-        tline_residual_c(P, c, rows, Xp, iy, iz, res);
-        double t[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int x = 0; x < TLX; ++x) {
-          if (x >= ex) break;
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) t[cx] += wt(Wx, cx, c.cext[0], ex, x) * res[x];
-        }
-        double wy[3], wz[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-        for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-          for (int cy = 0; cy < 3; ++cy) {
-            const double f = wy[cy] * wz[cz];
-#pragma unroll
-            for (int cx = 0; cx < 3; ++cx) r1[cx + 3 * (cy + 3 * cz)] += f * t[cx];
-          }
-      }
-      R.release();
-    }
-  }
-  if (valid) {
-    // z_1 = C r_1 (packed symmetric, fixed coarse box, interleaved by lane)
-    double z1[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) z1[k] = 0.0;
-    {
-      const double* C = P.Cp + w * 32ll * NPK + lane;
-      int idx = 0;
-#pragma unroll
-      for (int a = 0; a < NC; ++a) {
-#pragma unroll
-        for (int b = a; b < NC; ++b) {
-          const double cv = __ldcs(C + 32 * idx);
-          z1[a] += cv * r1[b];
-          if (b != a) z1[b] += cv * r1[a];
-          ++idx;
-        }
-      }
-    }
-    // y = x + P z_1, by lines
-    for (int kz = 0; kz < ez; ++kz) {
-      const int iz = wk.fz ? ez - 1 - kz : kz;
-      for (int ky = 0; ky < ey; ++ky) {
-        const int iy = wk.fy ? ey - 1 - ky : ky;
-        double wy[3], wz[3], u[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < 3; ++k) { wy[k] = wt(Wy, k, c.cext[1], ey, iy); wz[k] = wt(Wz, k, c.cext[2], ez, iz); }
-#pragma unroll
-        for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-          for (int cy = 0; cy < 3; ++cy) {
-            const double f = wy[cy] * wz[cz];
-#pragma unroll
-            for (int cx = 0; cx < 3; ++cx) u[cx] += f * z1[cx + 3 * (cy + 3 * cz)];
-          }
-        const long long f0 = (long long)(iz * ey + iy) * ex;
-#pragma unroll
-        for (int x = 0; x < TLX; ++x) {
-          if (x >= ex) break;
-          double e = 0.0;
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) e += wt(Wx, cx, c.cext[0], ex, x) * u[cx];
-          Yp[(f0 + x) * 32] = Xp[(f0 + x) * 32] + e;
-        }
-      }
-    }
-  }
-  // s = r - A y
-  for (int kz = 0; kz < ez; ++kz) {
-    const int iz = wk.fz ? ez - 1 - kz : kz;
-    for (int ky = 0; ky < ey; ++ky) {
-      const int iy = wk.fy ? ey - 1 - ky : ky;
-      const char* rows = R.wait(sline++) + rowoff;
-      if (valid) {
-        double res[TLX];
-        tline_residual_c(P, c, rows, Yp, iy, iz, res);
-        const long long f0 = (long long)(iz * ey + iy) * ex;
-#pragma unroll
-        for (int x = 0; x < TLX; ++x) {
-          if (x >= ex) break;
-          __stcs(Sp + (f0 + x) * 32, res[x]);
-        }
-      }
-      R.release();
-    }
-  }
-}
-
 // ------------------------------------------------------------------ smoothing phases
 // pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
 // post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
-// IW = 0: U-records (one schedule per warp); IW < 0: U-records whose columns have at most 7
-// pairs, -IW register stages; IW > 0: T-records with IW-byte node indices.
+// IW = 0: U-records (one schedule per warp), else T-records with IW-byte node indices.
 template <int DIM, bool POST, int IW>
 __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   constexpr int NP = DIM == 3 ? 13 : 4;
@@ -2033,7 +1186,6 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   tsm[VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
   if constexpr (IW == 0) usmooth(blk, tsm + lane, n0, P.pfd, lane);
-  else if constexpr (IW < 0) usmooth_p<7, -IW>(blk, tsm + lane, n0, P.pfd, lane);
   else tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
   __syncwarp();
   if (!POST) {
@@ -2061,8 +1213,6 @@ static TcParams make_tparams(const lorpc_prec* b, const double* r, double* z) {
   int acc = VO(b->max_n[0] + 1, 0);
   P.warp_doubles = (acc + 1) & ~1;
   P.pfd = getenv("LORPC_TPFD") ? atoi(getenv("LORPC_TPFD")) : 32;
-  // cooperative LOR rows in the middle phase: U-mode slot order (row runs), 3D, p <= 3
-  P.coop = b->umode && b->m->d == 3 && b->m->p <= 3 && getenv("LORPC_MID_COOP") && atoi(getenv("LORPC_MID_COOP")) != 0;
   return P;
 }
 
@@ -2080,40 +1230,7 @@ static int tlaunch(const TcParams& P, unsigned wblocks, unsigned mblocks, size_t
   k_vt_smooth<DIM, false, IW><<<wblocks, 32, smem, s>>>(P);
   LORPC_LAUNCHED();
   if constexpr (DIM == 3) {
-    // LOR rows through a cp.async ring (k_vt_mid3r), RD nodes deep: LORPC_MID_RD = 3, 4, 6, 8;
-    // 0 = the register-load line kernel k_vt_mid3l
-    static const int rd = getenv("LORPC_MID_RD") ? atoi(getenv("LORPC_MID_RD")) : 0;
-    if (lines && rd > 0) {
-      auto go = [&](auto kern, int RD) {
-        const int sm = RD * MSLOT;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        kern<<<wblocks, 32, sm, s>>>(P);
-      };
-      if (rd <= 3) go(k_vt_mid3r<3>, 3);
-      else if (rd == 4) go(k_vt_mid3r<4>, 4);
-      else if (rd <= 6) go(k_vt_mid3r<6>, 6);
-      else go(k_vt_mid3r<8>, 8);
-    } else if (lines && getenv("LORPC_MID_SMEM") && atoi(getenv("LORPC_MID_SMEM")) != 0) {
-      // patch vectors staged in shared memory (k_vt_mid3s): the smoothing kernels' footprint + one mbarrier
-      const size_t sm = smem + 64;
-      cudaFuncSetAttribute(k_vt_mid3s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_vt_mid3s, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      k_vt_mid3s<<<wblocks, 32, sm, s>>>(P);
-    } else if (lines && P.coop) {
-      static const int nbuf = getenv("LORPC_MID_NBUF") ? atoi(getenv("LORPC_MID_NBUF")) : 2;
-      auto go = [&](auto kern, int NB) {
-        const int sm = NB * (CROWS * CROWP) + 64;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        kern<<<wblocks, 32, sm, s>>>(P);
-      };
-      if (nbuf <= 1) go(k_vt_mid3c<1>, 1);
-      else if (nbuf == 2) go(k_vt_mid3c<2>, 2);
-      else go(k_vt_mid3c<3>, 3);
-      LORPC_LAUNCHED();
-      k_vt_mid3l<<<mblocks, 128, 0, s>>>(P);
-    } else if (lines) k_vt_mid3l<<<mblocks, 128, 0, s>>>(P);
+    if (lines) k_vt_mid3l<<<mblocks, 128, 0, s>>>(P);
     else k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
   } else {
     k_vt_mid<2><<<mblocks, 128, 0, s>>>(P);
@@ -2134,15 +1251,8 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
   const unsigned wblocks = (unsigned)(P.nslots / 32), mblocks = (unsigned)((P.nslots + 127) / 128);
   if (b->umode) {
-    // register stages of the U sweeps (LORPC_UNST = 2: the 13-pair two-stage sweeps)
-    static const int unst = getenv("LORPC_UNST") ? atoi(getenv("LORPC_UNST")) : 2;
-    const bool lines = b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE");
     if (b->m->d == 2) LORPC_TRY((tlaunch<2, 0>(P, wblocks, mblocks, smem, s, false)));
-    else if (b->umpmax <= 7 && unst == 3) LORPC_TRY((tlaunch<3, -3>(P, wblocks, mblocks, smem, s, lines)));
-    else if (b->umpmax <= 7 && unst == 4) LORPC_TRY((tlaunch<3, -4>(P, wblocks, mblocks, smem, s, lines)));
-    else if (b->umpmax <= 7 && unst == 5) LORPC_TRY((tlaunch<3, -5>(P, wblocks, mblocks, smem, s, lines)));
-    else if (b->umpmax <= 7 && unst >= 6) LORPC_TRY((tlaunch<3, -6>(P, wblocks, mblocks, smem, s, lines)));
-    else LORPC_TRY((tlaunch<3, 0>(P, wblocks, mblocks, smem, s, lines)));
+    else LORPC_TRY((tlaunch<3, 0>(P, wblocks, mblocks, smem, s, b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE"))));
   } else if (b->m->d == 2) {
     if (tiw(P.n0max) == 1) LORPC_TRY((tlaunch<2, 1>(P, wblocks, mblocks, smem, s, false)));
     else LORPC_TRY((tlaunch<2, 2>(P, wblocks, mblocks, smem, s, false)));
