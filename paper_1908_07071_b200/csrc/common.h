@@ -129,6 +129,7 @@ struct lorpc_prec {
   // thread-per-patch V-cycle (vcycle_t.cu): warp-interleaved factors, parking buffer
   bool tmode = false;
   bool umode = false;               // thread mode with one shared sweep schedule per warp (U-records)
+  int umpmax = 13;                  // widest column (pairs) of the U-records
   long long tslots = 0;             // warp slots of pord (multiple of 32)
   char* trec = nullptr;
   long long* trecoff = nullptr;

@@ -62,8 +62,11 @@ __device__ __forceinline__ void ldg256(const double* p, double (&v)[4]) {
 //     component when Q = 4), transposed x contraction                   [T2^T]
 //   y-lines: transposed y contraction                                   [T1^T]
 //   z-lines: transposed z contraction, scatter-add (atomics; free nodes only).
+#ifndef LORPC_CG3_MINB
+#define LORPC_CG3_MINB 6  // CTAs per SM asked of ptxas at p = 3 (measured on C5: 6 -> 1.64 ms, 7 (72 registers, spills) -> 1.88 ms, 8 -> 2.04 ms)
+#endif
 template <int P, int EB>
-__global__ void __launch_bounds__((P + 1) * (P + 1) * EB)
+__global__ void __launch_bounds__((P + 1) * (P + 1) * EB, (P == 3 ? LORPC_CG3_MINB : 1))
 k_cg3(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ G, int3 n, int3 N,
       const __grid_constant__ Basis1D bs, long long e0, long long e1, double* __restrict__ xy_part) {
   constexpr int Q = P + 1, Q2 = Q * Q, Q3 = Q * Q * Q;

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
   double* Dd = fill ? (double*)(blk + U.D) : nullptr;
   double* Lc = fill ? (double*)(blk + U.Lc) : nullptr;
   bool mism = valid && n != S;
-  int kp = 0;
+  int kp = 0, mpw = 0;
   for (int t = 0; t < S; ++t) {
     int node = 0, b0 = 0, cb = 0;
     if (valid && t < n) { node = sch[t]; b0 = brp[t]; cb = brp[t + 1] - b0; }
@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
     if (valid && (node != rnode || cb != rcb)) mism = true;
     const int mp = (rcb + 1) / 2;
     if (mp > UMP) mism = true;
+    if (mp > mpw) mpw = mp;
     for (int k = 0; k < rcb && k < 2 * UMP; ++k) {
       const int nd = (valid && k < cb) ? bkv[b0 + k] : 0;
       const int rnd = __shfl_sync(0xffffffffu, nd, ref);
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(128) k_urec(TRecParams P, long long nslots, in
   }
   if (kp > 65535) mism = true;
   if (__any_sync(0xffffffffu, mism) && lane == 0) atomicExch(bad, 1);
+  if (!fill && lane == 0) atomicMax(bad + 1, mpw);  // widest column (pairs) of any warp
   if (!fill && lane == 0) P.sizes[w] = urec_layout(S, kp).total;
   if (fill && lane == 0) *(int4*)blk = make_int4(S, kp, 0, 0);
 }
@@ -337,17 +339,19 @@ static int urec_build(lorpc_prec* b, int TX, int TY, cudaStream_t s, int* ok) {
   long long* sizes = nullptr;
   int* bad = nullptr;
   LORPC_TRY(dalloc(&sizes, (size_t)nw));
-  LORPC_TRY(dalloc(&bad, 1));
-  LORPC_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  LORPC_TRY(dalloc(&bad, 2));
+  LORPC_CUDA(cudaMemsetAsync(bad, 0, 2 * sizeof(int), s));
   P.sizes = sizes;
   const unsigned blocks = (unsigned)((nslots + 127) / 128);
   k_urec<<<blocks, 128, 0, s>>>(P, nslots, 0, bad);
   LORPC_LAUNCHED();
   std::vector<long long> h((size_t)nw);
-  int hbad = 0;
+  int hbad2[2] = {0, 0};
   LORPC_CUDA(cudaMemcpyAsync(h.data(), sizes, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, s));
-  LORPC_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LORPC_CUDA(cudaMemcpyAsync(hbad2, bad, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   LORPC_CUDA(cudaStreamSynchronize(s));
+  const int hbad = hbad2[0];
+  b->umpmax = hbad2[1];
   if (hbad) {
     dfree(sizes); dfree(bad); dfree(b->pord);
     b->pord = nullptr;
@@ -679,21 +683,24 @@ __device__ __forceinline__ int ump(const UDesc& d) { return (d.w[0] >> 8) & 0xff
 __device__ __forceinline__ int ukp(const UDesc& d) { return (int)(d.w[0] >> 16); }
 __device__ __forceinline__ int unb(const UDesc& d, int m) { return (d.w[1 + (m >> 2)] >> (8 * (m & 3))) & 0xff; }
 
+template <int MPT>
 struct UStage {
-  double2 l[UMP];
+  double2 l[MPT];
   double dinv;
 };
-template <bool BWD>
-__device__ __forceinline__ void uload(UStage& g, const UDesc& d, const double2* __restrict__ Lp,
+// the step's column: MPT predicated loads off one base address (rows of 512 bytes)
+template <bool BWD, int MPT>
+__device__ __forceinline__ void uload(UStage<MPT>& g, const UDesc& d, const double2* __restrict__ Lp,
                                       const double* __restrict__ Dd, int t) {
-  const int mp = ump(d), kp = ukp(d);
+  const int mp = ump(d);
+  const double2* base = Lp + (long long)ukp(d) * 32;
 #pragma unroll
-  for (int p = 0; p < UMP; ++p)
-    if (p < mp) g.l[p] = LORPC_RLD(Lp + (long long)(kp + p) * 32);
+  for (int p = 0; p < MPT; ++p)
+    if (p < mp) g.l[p] = LORPC_RLD(base + p * 32);
   if (!BWD) g.dinv = LORPC_RLD(Dd + 32 * t);
 }
-template <int MP>
-__device__ __forceinline__ void ufwd(const UStage& g, const UDesc& d, double* X) {
+template <int MP, class G>
+__device__ __forceinline__ void ufwd(const G& g, const UDesc& d, double* X) {
   const int k = unode(d);
   const double yk = X[LORPC_XS * k];
   double v[2 * MP + 1];
@@ -706,8 +713,8 @@ __device__ __forceinline__ void ufwd(const UStage& g, const UDesc& d, double* X)
   }
   X[LORPC_XS * k] = yk * g.dinv;
 }
-template <int MP>
-__device__ __forceinline__ void ubwd(const UStage& g, const UDesc& d, double* X) {
+template <int MP, class G>
+__device__ __forceinline__ void ubwd(const G& g, const UDesc& d, double* X) {
   const int k = unode(d);
   double a[4] = {X[LORPC_XS * k], 0.0, 0.0, 0.0};
 #pragma unroll
@@ -717,12 +724,13 @@ __device__ __forceinline__ void ubwd(const UStage& g, const UDesc& d, double* X)
   }
   X[LORPC_XS * k] = (a[0] + a[1]) + (a[2] + a[3]);
 }
-template <bool BWD, int MP>
-__device__ __forceinline__ void ustep_mp(const UStage& g, const UDesc& d, double* X) {
+template <bool BWD, int MP, class G>
+__device__ __forceinline__ void ustep_mp(const G& g, const UDesc& d, double* X) {
   if (BWD) ubwd<MP>(g, d, X); else ufwd<MP>(g, d, X);
 }
-template <bool BWD>
-__device__ __forceinline__ void ustep(const UStage& g, const UDesc& d, double* X) {
+template <bool BWD, int MPT>
+__device__ __forceinline__ void ustep(const UStage<MPT>& g, const UDesc& d, double* X) {
+  constexpr int M = MPT;
   switch (ump(d)) {  // warp-uniform
     case 0: ustep_mp<BWD, 0>(g, d, X); break;
     case 1: ustep_mp<BWD, 1>(g, d, X); break;
@@ -732,15 +740,15 @@ __device__ __forceinline__ void ustep(const UStage& g, const UDesc& d, double* X
     case 5: ustep_mp<BWD, 5>(g, d, X); break;
     case 6: ustep_mp<BWD, 6>(g, d, X); break;
     case 7: ustep_mp<BWD, 7>(g, d, X); break;
-    case 8: ustep_mp<BWD, 8>(g, d, X); break;
-    case 9: ustep_mp<BWD, 9>(g, d, X); break;
-    case 10: ustep_mp<BWD, 10>(g, d, X); break;
-    case 11: ustep_mp<BWD, 11>(g, d, X); break;
-    case 12: ustep_mp<BWD, 12>(g, d, X); break;
-    default: ustep_mp<BWD, 13>(g, d, X); break;
+    case 8: if (M >= 8) ustep_mp<BWD, (M >= 8 ? 8 : 0)>(g, d, X); break;
+    case 9: if (M >= 9) ustep_mp<BWD, (M >= 9 ? 9 : 0)>(g, d, X); break;
+    case 10: if (M >= 10) ustep_mp<BWD, (M >= 10 ? 10 : 0)>(g, d, X); break;
+    case 11: if (M >= 11) ustep_mp<BWD, (M >= 11 ? 11 : 0)>(g, d, X); break;
+    case 12: if (M >= 12) ustep_mp<BWD, (M >= 12 ? 12 : 0)>(g, d, X); break;
+    default: if (M >= 13) ustep_mp<BWD, (M >= 13 ? 13 : 0)>(g, d, X); break;
   }
 }
-template <bool BWD>
+template <bool BWD, int MPT>
 __device__ __forceinline__ void usweep(const char* __restrict__ blk, double* X, int TPFD, int lane) {
   const int4 hd = __ldg((const int4*)blk);
   const int S = hd.x, E2 = hd.y;
@@ -774,27 +782,28 @@ __device__ __forceinline__ void usweep(const char* __restrict__ blk, double* X, 
     }
   };
   UDesc dA, dB, dN;
-  UStage A, B;
+  UStage<MPT> A, B;
   uload_desc(dA, Dsc + 2 * st(0));
   if (S > 1) uload_desc(dB, Dsc + 2 * st(1));
-  uload<BWD>(A, dA, Lp, Dd, st(0));
+  uload<BWD, MPT>(A, dA, Lp, Dd, st(0));
   for (int q = 0; q < S; q += 2) {
     prefetch(dA);
-    if (q + 1 < S) uload<BWD>(B, dB, Lp, Dd, st(q + 1));
+    if (q + 1 < S) uload<BWD, MPT>(B, dB, Lp, Dd, st(q + 1));
     if (q + 2 < S) uload_desc(dN, Dsc + 2 * st(q + 2));
-    ustep<BWD>(A, dA, X);
+    ustep<BWD, MPT>(A, dA, X);
     if (q + 1 >= S) break;
     dA = dN;
-    if (q + 2 < S) uload<BWD>(A, dA, Lp, Dd, st(q + 2));
+    if (q + 2 < S) uload<BWD, MPT>(A, dA, Lp, Dd, st(q + 2));
     if (q + 3 < S) uload_desc(dN, Dsc + 2 * st(q + 3));
-    ustep<BWD>(B, dB, X);
+    ustep<BWD, MPT>(B, dB, X);
     dB = dN;
   }
 }
+template <int MPT>
 __device__ __forceinline__ void usmooth(const char* __restrict__ blk, double* X, int dummy, int TPFD, int lane) {
-  usweep<false>(blk, X, TPFD, lane);
+  usweep<false, MPT>(blk, X, TPFD, lane);
   X[LORPC_XS * dummy] = 0.0;
-  usweep<true>(blk, X, TPFD, lane);
+  usweep<true, MPT>(blk, X, TPFD, lane);
 }
 
 // ------------------------------------------------------------------ middle phase
@@ -1151,7 +1160,8 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
 // ------------------------------------------------------------------ smoothing phases
 // pre (POST = false): X = r_j (gather), X = M^{-1} X, x -> xpark.
 // post (POST = true): X = s (spark), X = M^{-1} X, z += I_j (y + X) (a8).
-// IW = 0: U-records (one schedule per warp), else T-records with IW-byte node indices.
+// IW = 0: U-records (one schedule per warp); IW = -1: U-records whose columns have at most 7
+// pairs (smaller register stages and dispatch); IW > 0: T-records with IW-byte node indices.
 template <int DIM, bool POST, int IW>
 __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   constexpr int NP = DIM == 3 ? 13 : 4;
@@ -1178,15 +1188,30 @@ __global__ void __launch_bounds__(32) k_vt_smooth(TcParams P) {
   };
   const long long col = w * (long long)n0 * 32 + lane;
   if (!POST) {
-    for (int i = 0; i < n0; ++i)  // r_j = I_j^T r (a5)
-      tsm[VO(i, lane)] = (valid && i < c.n) ? __ldg(P.r + gidx(i)) : 0.0;
+    // r_j = I_j^T r (a5): the box is walked x-fastest, its global index kept incrementally
+    long long g = (long long)c.lo[0] + Nx * (c.lo[1] + Ny * (long long)(DIM == 3 ? c.lo[2] : 0));
+    int ix = 0, iy = 0;
+    for (int i = 0; i < n0; ++i) {
+      const bool in = valid && i < c.n;
+      tsm[VO(i, lane)] = in ? __ldg(P.r + g) : 0.0;
+      ++g;
+      if (++ix == c.ext[0]) {
+        ix = 0; g += Nx - c.ext[0];
+        if (++iy == c.ext[1]) { iy = 0; g += Nx * (Ny - c.ext[1]); }
+      }
+    }
   } else {
     for (int i = 0; i < n0; ++i) tsm[VO(i, lane)] = __ldcs(P.spark + col + i * 32);
   }
   tsm[VO(n0, lane)] = 0.0;  // dummy node of the padded sweep steps
   __syncwarp();
-  if constexpr (IW == 0) usmooth(blk, tsm + lane, n0, P.pfd, lane);
-  else tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
+  if constexpr (IW == 0) {
+    usmooth<UMP>(blk, tsm + lane, n0, P.pfd, lane);
+  } else if constexpr (IW < 0) {  // U-records whose columns have at most 7 pairs
+    usmooth<7>(blk, tsm + lane, n0, P.pfd, lane);
+  } else {
+    tsmooth<NP, IW>(blk, tsm + lane, n0, P.pfd, lane);
+  }
   __syncwarp();
   if (!POST) {
     for (int i = 0; i < n0; ++i) __stcs(P.xpark + col + i * 32, tsm[VO(i, lane)]);
@@ -1251,8 +1276,10 @@ int vcycle_t_apply(const lorpc_prec* b, const double* r, double* z, cudaStream_t
   if (smem > 227 * 1024) return fail(LORPC_ERR_SIZE, "vcycle_t: warp vectors do not fit in shared memory");
   const unsigned wblocks = (unsigned)(P.nslots / 32), mblocks = (unsigned)((P.nslots + 127) / 128);
   if (b->umode) {
+    const bool lines = b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE");
     if (b->m->d == 2) LORPC_TRY((tlaunch<2, 0>(P, wblocks, mblocks, smem, s, false)));
-    else LORPC_TRY((tlaunch<3, 0>(P, wblocks, mblocks, smem, s, b->m->p <= 3 && !getenv("LORPC_MID_NODEWISE"))));
+    else if (b->umpmax <= 7 && !getenv("LORPC_UMP13")) LORPC_TRY((tlaunch<3, -1>(P, wblocks, mblocks, smem, s, lines)));
+    else LORPC_TRY((tlaunch<3, 0>(P, wblocks, mblocks, smem, s, lines)));
   } else if (b->m->d == 2) {
     if (tiw(P.n0max) == 1) LORPC_TRY((tlaunch<2, 1>(P, wblocks, mblocks, smem, s, false)));
     else LORPC_TRY((tlaunch<2, 2>(P, wblocks, mblocks, smem, s, false)));
