@@ -837,8 +837,20 @@ __device__ __forceinline__ void tweights(const TcParams& P, const TPatch& c, int
 // one 256-bit load (LDG.E.ENL2.256): a lane-per-patch walk reads a different row in
 // every lane, so each warp load costs one L1 wavefront per lane; four doubles per
 // load halve the wavefronts of 16-byte loads
+// LORPC_ROW_HINT: cache priority of the LOR rows (shared by neighbouring patches, against the
+// streaming patch vectors and coarse operators): 0 none, 1 L2 evict-last, 2 L1 + L2 evict-last
+#ifndef LORPC_ROW_HINT
+#define LORPC_ROW_HINT 0
+#endif
 __device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
+#if LORPC_ROW_HINT == 1
+  asm volatile("ld.global.nc.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+#elif LORPC_ROW_HINT == 2
+  asm volatile("ld.global.nc.L1::evict_last.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+#else
   asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+#endif
 }
 
 // s_i = r_i - (A_0 v)_i at node i of the lane's patch, v = the lane's column V
@@ -991,6 +1003,15 @@ __global__ void __launch_bounds__(128) k_vt_mid(TcParams P) {
 // 256-bit loads) and 27 FMAs instead of 27 predicated vector loads; restriction and
 // prolongation are separable per line (3 FMAs per node, 27 per line).
 constexpr int TLX = 5;  // largest box extent of the line variant
+// park-buffer accesses of the line kernel: the patch vectors stream through once, the LOR
+// rows are shared by neighbouring patches; LORPC_PARK_STREAM=1 marks the former evict-first
+#ifdef LORPC_PARK_STREAM
+#define LORPC_PLD(p) __ldcs(p)
+#define LORPC_PST(p, v) __stcs(p, v)
+#else
+#define LORPC_PLD(p) (*(p))
+#define LORPC_PST(p, v) (*(p) = (v))
+#endif
 template <bool RESTRICT>
 __device__ __forceinline__ void tline_residual(const TcParams& P, const TPatch& c, const double* __restrict__ V,
                                                int iy, int iz, double* res) {
@@ -1016,7 +1037,7 @@ __device__ __forceinline__ void tline_residual(const TcParams& P, const TPatch& 
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy) {
       W[dz][dy][0] = 0.0;
-      W[dz][dy][1] = ok[dz][dy] ? L[dz][dy][0] : 0.0;
+      W[dz][dy][1] = ok[dz][dy] ? LORPC_PLD(L[dz][dy]) : 0.0;
     }
 #pragma unroll
   for (int x = 0; x < TLX; ++x) {
@@ -1025,7 +1046,7 @@ __device__ __forceinline__ void tline_residual(const TcParams& P, const TPatch& 
     for (int dz = 0; dz < 3; ++dz)
 #pragma unroll
       for (int dy = 0; dy < 3; ++dy)
-        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? L[dz][dy][(x + 1) * 32] : 0.0;
+        W[dz][dy][x + 2] = (ok[dz][dy] && x + 1 < ex) ? LORPC_PLD(L[dz][dy] + (x + 1) * 32) : 0.0;
     const long long gi = g0 + x;
     const double* Ar = P.A0 + (size_t)gi * 28;
     double a0 = __ldg(P.r + gi), a1 = 0.0;
@@ -1136,7 +1157,7 @@ __global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
         double e = 0.0;
 #pragma unroll
         for (int cx = 0; cx < 3; ++cx) e += wt(Wx, cx, c.cext[0], ex, x) * u[cx];
-        Yp[(f0 + x) * 32] = Xp[(f0 + x) * 32] + e;
+        LORPC_PST(Yp + (f0 + x) * 32, LORPC_PLD(Xp + (f0 + x) * 32) + e);
       }
     }
   }
