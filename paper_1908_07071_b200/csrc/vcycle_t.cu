@@ -1067,7 +1067,13 @@ __device__ __forceinline__ void tline_residual(const TcParams& P, const TPatch& 
   }
 }
 
-__global__ void __launch_bounds__(128) k_vt_mid3l(TcParams P) {
+#ifndef LORPC_MID3L_MINB
+#define LORPC_MID3L_MINB 1  // CTAs of 4 warps per SM asked of ptxas (1: 254 registers, 8 warps per SM)
+#endif
+#ifndef LORPC_MID3L_THREADS
+#define LORPC_MID3L_THREADS 128  // consecutive warps (patch rows of a tile layer) per CTA
+#endif
+__global__ void __launch_bounds__(LORPC_MID3L_THREADS, LORPC_MID3L_MINB) k_vt_mid3l(TcParams P) {
   constexpr int NC = 27, NPK = TCoarse<3>::NPK;
   const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (slot >= P.nslots) return;
@@ -1276,7 +1282,7 @@ static int tlaunch(const TcParams& P, unsigned wblocks, unsigned mblocks, size_t
   k_vt_smooth<DIM, false, IW><<<wblocks, 32, smem, s>>>(P);
   LORPC_LAUNCHED();
   if constexpr (DIM == 3) {
-    if (lines) k_vt_mid3l<<<mblocks, 128, 0, s>>>(P);
+    if (lines) k_vt_mid3l<<<(unsigned)((P.nslots + LORPC_MID3L_THREADS - 1) / LORPC_MID3L_THREADS), LORPC_MID3L_THREADS, 0, s>>>(P);
     else k_vt_mid<3><<<mblocks, 128, 0, s>>>(P);
   } else {
     k_vt_mid<2><<<mblocks, 128, 0, s>>>(P);

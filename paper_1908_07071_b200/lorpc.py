@@ -213,7 +213,7 @@ class Prec:
     KERNELS = {0: "group-mode patch V-cycle (k_vcycle, every level in shared memory)",
                1: "thread-mode patch V-cycle (k_vt_smooth pre + k_vt_mid + k_vt_smooth post)",
                2: "W-mode fused patch V-cycle (k_vw, factor staged in shared memory)",
-               3: "thread-mode patch V-cycle, one sweep schedule per warp (U-records: k_vt_smooth<.,.,0> pre + k_vt_mid + post)",
+               3: "thread-mode patch V-cycle, one sweep schedule per warp (U-records: k_vt_smooth pre + k_vt_mid3l / k_vt_mid + k_vt_smooth post)",
                4: "Q-mode fused patch V-cycle (k_vq: LP lanes per patch, factors streamed through a cp.async ring)"}
 
     def kernel(self):
