@@ -368,7 +368,7 @@ def run_lorpc_dist(args, cfg, dev, rank, world, dist):
     dist.broadcast(idt, 0)
     t0 = time.perf_counter()
     V = vertices(cfg)
-    D = L.Dist(cfg.n, cfg.p, V, world, rank=rank, nccl_id=bytes(idt.cpu().numpy().tobytes()))
+    D = L.Dist(cfg.n, cfg.p, V, world, rank=rank, nccl_id=bytes(idt.cpu().numpy().tobytes()), ordering=args.ordering)
     off, cnt, npatch = D.owned[0]
     b_host = random_free_rhs(cfg)[off:off + cnt] if cfg.rhs == "randn" else None
     assert b_host is not None, "multi-GPU bench uses the C5 random-RHS recipe"
@@ -441,8 +441,9 @@ def run_lorpc_dist(args, cfg, dev, rank, world, dist):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded workloads/ generators)",
                 "config": {"workload": f"{cfg.name}: 3D CG {'x'.join(map(str, cfg.n))} p={cfg.p}, perturb={cfg.perturb}h, "
+                                       f"vertex patches, {args.ordering.upper()}-ILU(0) V(1,1), GMG R_0, "
                                        f"z-slabs over {world} GPUs, NCCL halo exchange, tol={cfg.tol}",
-                           "n_dof": n_dof, "pcg_iters_per_solve": iters[0], "setup_s": round(t_setup, 3),
+                           "ordering": args.ordering, "n_dof": n_dof, "pcg_iters_per_solve": iters[0], "setup_s": round(t_setup, 3),
                            "parallelism": f"slab{world}", "patches_rank0": npatch,
                            "l2": "inputs larger than L2 (working set >> 126 MB)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -92,6 +92,41 @@ def test_dist_matches_single(L, n, p, R):
     assert rel(xd, xo) < 1e-9
 
 
+@pytest.mark.parametrize("n,p,R", [((4, 3, 5), 3, 2), ((4, 3, 8), 3, 8), ((3, 3, 4), 2, 4)])
+def test_dist_rcm_matches_single(L, n, p, R):
+    """The slab path with a structure-only ordering (RCM: the ranks' patch subsets run the
+    U-record kernels, bench default of C5): preconditioner equal to the single-rank path,
+    PCG iterations +-1 vs the single rank and the oracle."""
+    cfg = small_config("C5", n, p=p)
+    V = vertices(cfg)
+    mesh = L.Mesh(3, cfg.n, p, V)
+    prec = L.Prec(L.Lor(mesh), ordering="rcm")
+    D = L.Dist(cfg.n, p, V, R, ordering="rcm")
+    N = mesh.n_dof
+    P = O.Problem.from_config(cfg)
+    X = P.node_coords()
+    r = parity_vector(N)
+    r[~np.all((X > 1e-12) & (X < 1 - 1e-12), axis=1)] = 0.0
+    z1 = torch.empty(N, dtype=torch.float64, device="cuda")
+    prec.apply(dev(r), z1)
+    zs = [torch.empty_like(t) for t in split(D, r)]
+    D.precond(split(D, r), zs)
+    torch.cuda.synchronize()
+    assert rel(join(D, zs, N), z1.cpu().numpy()) < 1e-12
+    b = random_free_rhs(cfg)
+    x1 = torch.empty(N, dtype=torch.float64, device="cuda")
+    rep1 = L.pcg_solve(mesh, prec, dev(b), x1, cfg.tol)
+    xs = [torch.empty_like(t) for t in split(D, b)]
+    repd = D.pcg_solve(split(D, b), xs, cfg.tol)
+    xd = join(D, xs, N)
+    assert abs(repd["iters"] - rep1["iters"]) <= 1, (repd["iters"], rep1["iters"])
+    assert rel(xd, x1.cpu().numpy()) < 1e-9
+    P.schwarz_setup("vertex", "rcm", "gmg")
+    xo, ro = P.pcg(b, cfg.tol)
+    assert abs(repd["iters"] - ro["iters"]) <= 1, (repd["iters"], ro["iters"])
+    assert rel(xd, xo) < 1e-9
+
+
 def test_dist_rejects_bad_partition(L):
     cfg = small_config("C5", (3, 3, 2), p=3)
     with pytest.raises(L.LorpcError):
